@@ -1,0 +1,110 @@
+// Host launchers of the B200 multigrid kernels (pmg_kernels.cu, pmg_setup.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "pmg_common.cuh"
+
+namespace pmg {
+
+// Envelope LDL^T of the across-origin ring in antipodally interleaved order
+// (reference smoother.cpp:33-49, line_algebra.cpp:122-255).  Rows < n-2
+// have bandwidth <= 2; the two closing rows are dense (Moebius ladder).
+struct OriginFactor {
+    const double* band1;  // [B][n] L(i,i-1)
+    const double* band2;  // [B][n] L(i,i-2)
+    const double* row1;   // [B][n] L(n-2,k), k in [fc1, n-2)
+    const double* row2;   // [B][n] L(n-1,k), k in [fc2, n-1)
+    const double* D;      // [B][n] LDL^T diagonal
+    int fc1, fc2;
+};
+
+// Generic envelope factor with identity ordering (coarsest level).
+struct EnvFactor {
+    const int* fc;      // [n] first column per row
+    const long* ro;     // [n+1] row offsets into L
+    const double* L;    // [B][nnz]
+    const double* D;    // [B][n]
+    long nnz;
+    int n;
+};
+
+struct Weights {  // transfer weights of a fine level (interpolation.cpp:19-36)
+    const double* rwb;  // [nr] radial_weight_below(sf) (odd sf)
+    const double* rwa;  // [nr] radial_weight_above(sf)
+    const double* awb;  // [nt] angular_weight_below(tf) (odd tf)
+    const double* awa;  // [nt] angular_weight_above(tf)
+};
+
+// kernel classes for launch accounting / profiling
+enum KernelKind {
+    KK_RESIDUAL = 0,
+    KK_CIRCLE = 1,
+    KK_RADIAL = 2,
+    KK_SMOOTH = 3,
+    KK_RESTRICT = 4,
+    KK_PROLONG = 5,
+    KK_COARSE = 6,
+    KK_NORM = 7,
+    KK_OTHER = 8,
+    KK_COUNT = 9
+};
+
+// y = A u (mode 0) or r = f - A u (mode 1); when partials != nullptr also
+// writes per-block sum of squares (norm_type 0/1) or max |r| (norm_type 2)
+// into partials[b * gridDim.x + block].  Returns the number of partial blocks.
+int launch_apply(const LevelView& L, bool onfly, int mode, const double* u, const double* f,
+                 double* out, double* partials, int norm_type, const int* active,
+                 cudaStream_t st);
+int apply_blocks(const LevelView& L);
+
+void launch_circle(const LevelView& L, bool onfly, double* u, const double* f, const double* cil,
+                   const double* cm, const double* corner, const OriginFactor& of, int parity,
+                   const int* active, cudaStream_t st);
+void launch_radial(const LevelView& L, bool onfly, double* u, const double* f, const double* ril,
+                   const double* rm, int parity, const int* active, cudaStream_t st);
+
+// mask: zero the coarse Dirichlet rows (mask_dirichlet_rows, multigrid.cpp:146-153)
+void launch_restrict(const LevelView& F, const LevelView& C, const Weights& w, const double* fr,
+                     double* cf, double* cu_zero, bool mask, const int* active, cudaStream_t st);
+void launch_prolong(const LevelView& F, const LevelView& C, const Weights& w, const double* cu,
+                    double* fu, bool add, const int* active, cudaStream_t st);
+void launch_coarse(const LevelView& L, const EnvFactor& E, const double* f, double* u,
+                   const int* active, cudaStream_t st);
+
+// per-section norm from partial block values
+void launch_norm_final(const double* partials, int nblk, int B, long n, int norm_type,
+                       double* norms, cudaStream_t st);
+// sum of squares / max partials of an arbitrary vector set [B][n]
+int launch_norm_partials(const double* v, long n, int B, int norm_type, double* partials,
+                         cudaStream_t st);
+
+// convergence bookkeeping after a residual norm (multigrid.cpp:321-340)
+struct ConvState {
+    double* r0;         // [B]
+    double* hist;       // [B][cap]
+    int* active;        // [B]
+    int* iters;         // [B]
+    int* converged;     // [B]
+    int* remaining;     // [1]
+    int cap;
+};
+void launch_check(const double* norms, ConvState cs, int B, int it, int max_it, double rel_tol,
+                  double abs_tol, cudaStream_t st);
+
+void launch_fill(double* p, long n, double v, cudaStream_t st);
+void launch_set_active(int* active, int* remaining, int B, cudaStream_t st);
+void launch_flush(double* buf, long n, cudaStream_t st);
+
+// ---- setup (pmg_setup.cu) ----
+// coefficient arrays [B][n]; returns via *bad (device int) when |det| < 1e-14
+void launch_coeffs(const LevelView& L, double* arr, double* art, double* att, double* det,
+                   int* bad, cudaStream_t st);
+// circle-line cyclic factors of rings [0, split) (ring 0 skipped when across-origin)
+void launch_factor_circle(const LevelView& L, bool onfly, double* cil, double* cm,
+                          double* corner, int* bad, cudaStream_t st);
+void launch_factor_radial(const LevelView& L, bool onfly, double* ril, double* rm, int* bad,
+                          cudaStream_t st);
+// f = A u on the finest level for seeded RHS (same as launch_apply mode 0)
+
+}  // namespace pmg

@@ -1,0 +1,1210 @@
+// Host side of the B200 multigrid solve path: level hierarchy in device
+// memory, the V/W/F cycle driver, and the extern "C" ABI of
+// include/polarmg_b200.h.  Mirrors reference polarmg::MultigridSolver
+// (multigrid.hpp:86-151, multigrid.cpp:61-357).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/polarmg_b200.h"
+#include "pmg_common.cuh"
+#include "pmg_grid.hpp"
+#include "pmg_kernels.h"
+
+namespace pmg {
+
+// ------------------------------------------------------------------ errors
+struct PmgError : std::runtime_error {
+    int code;
+    PmgError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+thread_local std::string g_err;
+
+#define PMG_CUDA(call)                                                                  \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            throw PmgError(PMG_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                                          " at " #call);                                \
+    } while (0)
+
+// --------------------------------------------- envelope LDL^T (host setup)
+// Restates reference SparseDirectFactor (line_algebra.cpp:122-209).
+struct Trip {
+    int row, col;
+    double v;
+};
+
+struct HostEnv {
+    int n = 0;
+    std::vector<int> perm, iperm, fc;
+    std::vector<long> ro;
+    std::vector<double> L, D;
+
+    void factor(int n_, const std::vector<Trip>& tr, const std::vector<int>& permutation) {
+        n = n_;
+        perm = permutation;
+        if (perm.empty()) {
+            perm.resize(n);
+            for (int i = 0; i < n; ++i) perm[i] = i;
+        }
+        iperm.assign(n, -1);
+        for (int k = 0; k < n; ++k) iperm[perm[k]] = k;
+        fc.resize(n);
+        for (int i = 0; i < n; ++i) fc[i] = i;
+        for (const Trip& t : tr) {
+            if (t.row < 0 || t.row >= n || t.col < 0 || t.col > t.row)
+                throw PmgError(PMG_EINVAL, "sparse factor: triplets must address the lower triangle");
+            const int pi = iperm[t.row], pj = iperm[t.col];
+            const int hi = std::max(pi, pj), lo = std::min(pi, pj);
+            fc[hi] = std::min(fc[hi], lo);
+        }
+        ro.assign(n + 1, 0);
+        for (int i = 0; i < n; ++i) ro[i + 1] = ro[i] + (i - fc[i]);
+        L.assign(ro[n], 0.0);
+        D.assign(n, 0.0);
+        std::vector<char> seen(n, 0);
+        for (const Trip& t : tr) {
+            const int pi = iperm[t.row], pj = iperm[t.col];
+            if (pi == pj) {
+                D[pi] += t.v;
+                seen[pi] = 1;
+            } else {
+                const int hi = std::max(pi, pj), lo = std::min(pi, pj);
+                L[ro[hi] + (lo - fc[hi])] += t.v;
+            }
+        }
+        for (int i = 0; i < n; ++i)
+            if (!seen[i])
+                throw PmgError(PMG_ERUNTIME,
+                               "sparse factor: structurally singular (missing diagonal at row " +
+                                   std::to_string(perm[i]) + ")");
+        double scale = 0.0;
+        for (int i = 0; i < n; ++i) scale = std::max(scale, std::abs(D[i]));
+        for (int i = 0; i < n; ++i) {
+            const int fi = fc[i];
+            double* ri = L.data() + ro[i] - fi;
+            for (int j = fi; j < i; ++j) {
+                const int fj = fc[j];
+                const double* rj = L.data() + ro[j] - fj;
+                const int k0 = std::max(fi, fj);
+                double sum = ri[j];
+                for (int k = k0; k < j; ++k) sum -= ri[k] * D[k] * rj[k];
+                ri[j] = sum / D[j];
+            }
+            double d = D[i];
+            for (int k = fi; k < i; ++k) d -= ri[k] * ri[k] * D[k];
+            if (std::abs(d) < 1e-14 * std::max(scale, 1.0))
+                throw PmgError(PMG_ERUNTIME,
+                               "sparse factor: zero pivot at row " + std::to_string(perm[i]));
+            D[i] = d;
+        }
+    }
+    double at(int i, int k) const {  // L(i,k) within the envelope, else 0
+        if (k < fc[i] || k >= i) return 0.0;
+        return L[ro[i] + (k - fc[i])];
+    }
+};
+
+// host coefficient provider (same transform() as the device)
+struct HostCoef {
+    const LevelView* L;
+    int b;
+    Coef operator()(int s, int t) const {
+        return transform(L->geo, L->alpha[(long)b * L->nr + s], L->r[s], L->sn[t], L->cs[t],
+                         nullptr);
+    }
+};
+
+// assemble_coo (stencil.cpp:355-373) of a node subset given in NODE indices
+static std::vector<Trip> assemble_coo(const LevelView& HL, const HostGrid& g, int b,
+                                      const std::vector<int>& nodes) {
+    std::vector<int> local(g.n(), -1);
+    for (std::size_t i = 0; i < nodes.size(); ++i) local[nodes[i]] = static_cast<int>(i);
+    std::vector<Trip> out;
+    out.reserve(nodes.size() * 6);
+    HostCoef cf{&HL, b};
+    for (std::size_t i = 0; i < nodes.size(); ++i) {
+        int s, t;
+        HL.node(nodes[i], s, t);
+        const Row R = make_row(HL, cf, s, t);
+        const int lr = static_cast<int>(i);
+        auto push = [&](int col, double v) {
+            const int lc = local[col];
+            if (lc >= 0 && lc <= lr) out.push_back({lr, lc, v});
+        };
+        const int p = g.idx(s, t);
+        if (R.ident) {
+            push(p, 1.0);
+            continue;
+        }
+        const int tm = HL.tminus(t), tp = HL.tplus(t);
+        push(p, R.d);
+        if (R.has_sm) push(g.idx(s - 1, t), R.sm);
+        if (R.has_sp) push(g.idx(s + 1, t), R.sp);
+        push(g.idx(s, tm), R.tm);
+        push(g.idx(s, tp), R.tp);
+        if (R.has_sm) {
+            push(g.idx(s - 1, tm), R.mm);
+            push(g.idx(s - 1, tp), R.mp);
+        }
+        if (R.has_sp) {
+            push(g.idx(s + 1, tm), R.pm);
+            push(g.idx(s + 1, tp), R.pp);
+        }
+        if (R.origin) push(g.idx(0, R.t2), R.ph);
+    }
+    return out;
+}
+
+// ------------------------------------------------------------------ solver
+struct Level {
+    HostGrid g;
+    LevelView v{};
+    std::vector<double> h_alpha, h_beta, h_sn, h_cs;
+    double *u = nullptr, *f = nullptr, *res = nullptr;
+    double *arr = nullptr, *art = nullptr, *att = nullptr, *det = nullptr;
+    double *cil = nullptr, *cm = nullptr, *corner = nullptr, *ril = nullptr, *rm = nullptr;
+    double *ob1 = nullptr, *ob2 = nullptr, *or1 = nullptr, *or2 = nullptr, *oD = nullptr;
+    int ofc1 = 0, ofc2 = 0;
+    Weights w{};
+    EnvFactor env{};
+    OriginFactor of() const { return OriginFactor{ob1, ob2, or1, or2, oD, ofc1, ofc2}; }
+};
+
+struct Solver {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    Geo geo{};
+    pmg_problem prob{};
+    pmg_settings set{};
+    int B = 1;
+    std::vector<double> scales;
+    double tol = 1e-12;
+    bool onfly = false;
+    std::vector<Level> lv;
+    std::vector<void*> allocs;
+    size_t bytes = 0;
+    // convergence state
+    double *norms = nullptr, *partials = nullptr, *r0 = nullptr, *hist = nullptr;
+    int *active = nullptr, *iters = nullptr, *conv = nullptr, *remaining = nullptr;
+    int* h_remaining = nullptr;
+    int hist_cap = 0;
+    int partial_cap = 0;
+    double* flush_buf = nullptr;
+    long flush_n = 0;
+    long long launches = 0;
+    bool prof = false;
+    struct Ev {
+        int kind;
+        cudaEvent_t a, b;
+    };
+    std::vector<Ev> evs;
+    std::vector<cudaEvent_t> ev_pool;
+    double prof_ms[KK_COUNT] = {};
+    long long prof_n[KK_COUNT] = {};
+    double setup_seconds = 0.0;
+    double last_solve_ms = 0.0;
+
+    ~Solver() {
+        cudaSetDevice(device);
+        if (stream) cudaStreamSynchronize(stream);
+        for (auto& e : evs) {
+            cudaEventDestroy(e.a);
+            cudaEventDestroy(e.b);
+        }
+        for (auto e : ev_pool) cudaEventDestroy(e);
+        for (void* p : allocs) cudaFree(p);
+        if (h_remaining) cudaFreeHost(h_remaining);
+        if (own_stream && stream) cudaStreamDestroy(stream);
+    }
+
+    template <class T>
+    T* alloc(size_t count, bool zero = true) {
+        void* p = nullptr;
+        const size_t nb = std::max<size_t>(count, 1) * sizeof(T);
+        PMG_CUDA(cudaMalloc(&p, nb));
+        allocs.push_back(p);
+        bytes += nb;
+        if (zero) PMG_CUDA(cudaMemsetAsync(p, 0, nb, stream));
+        return static_cast<T*>(p);
+    }
+    template <class T>
+    T* upload(const std::vector<T>& v) {
+        T* p = alloc<T>(v.size(), false);
+        if (!v.empty())
+            PMG_CUDA(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice,
+                                     stream));
+        return p;
+    }
+
+    // ---- kernel launch wrapper: counts launches, optional per-class timing
+    cudaEvent_t pool_event() {
+        if (!ev_pool.empty()) {
+            cudaEvent_t e = ev_pool.back();
+            ev_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        PMG_CUDA(cudaEventCreate(&e));
+        return e;
+    }
+    template <class F>
+    void run(int kind, int nlaunch, F&& fn) {
+        if (prof) {
+            Ev e{kind, pool_event(), pool_event()};
+            PMG_CUDA(cudaEventRecord(e.a, stream));
+            fn();
+            PMG_CUDA(cudaEventRecord(e.b, stream));
+            evs.push_back(e);
+            prof_n[kind] += nlaunch;
+        } else {
+            fn();
+        }
+        launches += nlaunch;
+    }
+    void collect_profile() {
+        if (evs.empty()) return;
+        PMG_CUDA(cudaStreamSynchronize(stream));
+        for (auto& e : evs) {
+            float ms = 0.f;
+            PMG_CUDA(cudaEventElapsedTime(&ms, e.a, e.b));
+            prof_ms[e.kind] += ms;
+            ev_pool.push_back(e.a);
+            ev_pool.push_back(e.b);
+        }
+        evs.clear();
+    }
+
+    // ------------------------------------------------------------ setup
+    void build(const pmg_grid& gp) {
+        const auto t0 = std::chrono::steady_clock::now();
+        tol = gp.pair_tolerance > 0.0 ? gp.pair_tolerance : 1e-12;
+        HostGrid g0;
+        if (gp.mode == 0)
+            g0 = uniform_grid(gp.R0, gp.Rmax, gp.n_r, gp.n_theta, tol);
+        else if (gp.mode == 1)
+            g0 = build_grid(gp.R0, gp.Rmax, gp.nr_exp, gp.ntheta_exp, gp.anisotropic_factor,
+                            gp.divide_by_2, tol);
+        else {
+            if (!gp.radii || !gp.angles || gp.n_r <= 0 || gp.n_theta <= 0)
+                throw PmgError(PMG_EINVAL, "explicit grid requires radii and angles");
+            g0 = make_grid(std::vector<double>(gp.radii, gp.radii + gp.n_r),
+                           std::vector<double>(gp.angles, gp.angles + gp.n_theta), tol);
+        }
+        std::vector<HostGrid> grids;
+        grids.push_back(std::move(g0));
+        while ((set.max_levels == 0 || static_cast<int>(grids.size()) < set.max_levels) &&
+               can_coarsen(grids.back(), tol))
+            grids.push_back(coarsen(grids.back(), tol));
+        const int L = static_cast<int>(grids.size());
+        lv.resize(L);
+        onfly = set.stencil_mode == 1 && !set.cache_geometry;
+        int* bad = alloc<int>(1);
+        for (int l = 0; l < L; ++l) {
+            Level& V = lv[l];
+            V.g = std::move(grids[l]);
+            setup_level(V, l == L - 1, bad);
+        }
+        // convergence state
+        hist_cap = std::max(set.max_iterations, 0) + 1;
+        norms = alloc<double>(B);
+        r0 = alloc<double>(B);
+        hist = alloc<double>((size_t)B * hist_cap);
+        active = alloc<int>(B);
+        iters = alloc<int>(B);
+        conv = alloc<int>(B);
+        remaining = alloc<int>(1);
+        partial_cap = std::max(apply_blocks(lv[0].v), 1024);
+        partials = alloc<double>((size_t)B * partial_cap);
+        PMG_CUDA(cudaMallocHost(&h_remaining, sizeof(int)));
+        PMG_CUDA(cudaStreamSynchronize(stream));
+        setup_seconds =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+
+    void setup_level(Level& V, bool coarsest, int* bad) {
+        const HostGrid& g = V.g;
+        const int nr = g.nr(), nt = g.nt();
+        V.h_sn.resize(nt);
+        V.h_cs.resize(nt);
+        for (int t = 0; t < nt; ++t) {  // level_cache.cpp:27-32
+            V.h_sn[t] = std::sin(g.th[t]);
+            V.h_cs[t] = std::cos(g.th[t]);
+        }
+        V.h_alpha.resize((size_t)B * nr);
+        V.h_beta.resize((size_t)B * nr);
+        for (int b = 0; b < B; ++b)
+            for (int s = 0; s < nr; ++s) {  // problem.cpp:86-94
+                const double r = g.r[s];
+                const double a = prob.alpha_coeff == 0
+                                     ? 1.0
+                                     : scales[b] * std::exp(-std::tanh(
+                                                       (r / prob.rmax - prob.alpha_jump) /
+                                                       prob.delta_r));
+                V.h_alpha[(size_t)b * nr + s] = a;
+                V.h_beta[(size_t)b * nr + s] = prob.beta_coeff == 0 ? 0.0 : 1.0 / a;
+            }
+        LevelView& v = V.v;
+        v.nr = nr;
+        v.nt = nt;
+        v.split = g.split;
+        v.len = nr - g.split;
+        v.n = nr * nt;
+        v.B = B;
+        v.boundary = set.boundary_mode;
+        v.r0 = g.r[0];
+        v.geo = geo;
+        v.r = upload(g.r);
+        v.h = upload(g.h);
+        v.k = upload(g.k);
+        v.sn = upload(V.h_sn);
+        v.cs = upload(V.h_cs);
+        v.alpha = upload(V.h_alpha);
+        v.beta = upload(V.h_beta);
+        const size_t N = (size_t)B * v.n;
+        V.u = alloc<double>(N);
+        V.f = alloc<double>(N);
+        V.res = alloc<double>(N);
+        // coefficients: stored for Take (and Give+cacheDomainGeometry); for
+        // on-the-fly Give a temporary set validates |det DF| once.
+        {
+            double* a = alloc<double>(N, false);
+            double* c = alloc<double>(N, false);
+            double* t_ = alloc<double>(N, false);
+            double* d = alloc<double>(N, false);
+            v.arr = a;
+            v.art = c;
+            v.att = t_;
+            v.det = d;
+            PMG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), stream));
+            launch_coeffs(v, a, c, t_, d, bad, stream);
+            check_bad(bad, "singular Jacobian: mapping degenerate at queried point");
+            if (onfly) {  // release: Give recomputes coefficients
+                release(a);
+                release(c);
+                release(t_);
+                release(d);
+                v.arr = v.art = v.att = v.det = nullptr;
+            }
+        }
+        if (!coarsest) {
+            if (!g.uniform_angles)
+                throw PmgError(PMG_ERUNTIME,
+                               "smoother split undefined: non-uniform angular spacing; a more "
+                               "general switching condition or overlapping smoothers would be "
+                               "needed");
+            if (nt > 8192 || v.len > 8192)
+                throw PmgError(PMG_EINVAL,
+                               "line length above 8192 is not supported by the on-chip line "
+                               "solver (n_theta and n_r - split must be <= 8192)");
+            if (nt < 3)
+                throw PmgError(PMG_EINVAL,
+                               "cyclic_tridiag_factor: need n >= 3 (corner would duplicate a band)");
+            V.cil = alloc<double>((size_t)B * v.split * nt, false);
+            V.cm = alloc<double>((size_t)B * v.split * nt, false);
+            V.corner = alloc<double>((size_t)B * v.split);
+            PMG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), stream));
+            launch_factor_circle(v, onfly, V.cil, V.cm, V.corner, bad, stream);
+            check_bad(bad, "cyclic core not positive definite after rank-one shift");
+            if (v.len > 0) {
+                V.ril = alloc<double>((size_t)B * nt * v.len, false);
+                V.rm = alloc<double>((size_t)B * nt * v.len, false);
+                PMG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), stream));
+                launch_factor_radial(v, onfly, V.ril, V.rm, bad, stream);
+                check_bad(bad, "not positive definite (radial line factor)");
+            }
+            if (set.boundary_mode == 0) setup_origin(V);
+            setup_weights(V);
+        } else {
+            setup_coarsest(V);
+        }
+    }
+
+    void release(double* p) {
+        auto it = std::find(allocs.begin(), allocs.end(), static_cast<void*>(p));
+        if (it != allocs.end()) {
+            PMG_CUDA(cudaStreamSynchronize(stream));
+            cudaFree(p);
+            allocs.erase(it);
+        }
+    }
+
+    void check_bad(int* bad, const char* msg) {
+        int hb = 0;
+        PMG_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        PMG_CUDA(cudaStreamSynchronize(stream));
+        PMG_CUDA(cudaGetLastError());
+        if (hb) throw PmgError(PMG_ERUNTIME, msg);
+    }
+
+    LevelView host_view(const Level& V) const {
+        LevelView h = V.v;
+        h.r = V.g.r.data();
+        h.h = V.g.h.data();
+        h.k = V.g.k.data();
+        h.sn = V.h_sn.data();
+        h.cs = V.h_cs.data();
+        h.alpha = V.h_alpha.data();
+        h.beta = V.h_beta.data();
+        h.arr = h.art = h.att = h.det = nullptr;
+        return h;
+    }
+
+    // across-origin ring: envelope LDL^T in antipodal order (smoother.cpp:33-49)
+    void setup_origin(Level& V) {
+        const int nt = V.g.nt();
+        const LevelView HL = host_view(V);
+        std::vector<int> nodes(nt), perm(nt);
+        for (int t = 0; t < nt; ++t) nodes[t] = t;
+        for (int i = 0; i < nt / 2; ++i) {
+            perm[2 * i] = i;
+            perm[2 * i + 1] = nt / 2 + i;
+        }
+        std::vector<double> b1((size_t)B * nt, 0.0), b2((size_t)B * nt, 0.0),
+            r1((size_t)B * nt, 0.0), r2((size_t)B * nt, 0.0), D((size_t)B * nt, 0.0);
+        for (int b = 0; b < B; ++b) {
+            HostEnv E;
+            E.factor(nt, assemble_coo(HL, V.g, b, nodes), perm);
+            for (int i = 0; i < nt - 2; ++i)
+                if (E.fc[i] < i - 2)
+                    throw PmgError(PMG_ERUNTIME,
+                                   "origin ring factor: unexpected envelope structure");
+            if (b == 0) {
+                V.ofc1 = E.fc[nt - 2];
+                V.ofc2 = E.fc[nt - 1];
+            } else if (V.ofc1 != E.fc[nt - 2] || V.ofc2 != E.fc[nt - 1]) {
+                throw PmgError(PMG_ERUNTIME, "origin ring factor: section structures differ");
+            }
+            const size_t o = (size_t)b * nt;
+            for (int i = 0; i < nt; ++i) {
+                D[o + i] = E.D[i];
+                if (i < nt - 2) {
+                    b1[o + i] = E.at(i, i - 1);
+                    b2[o + i] = E.at(i, i - 2);
+                }
+            }
+            for (int k = 0; k < nt - 2; ++k) r1[o + k] = E.at(nt - 2, k);
+            for (int k = 0; k < nt - 1; ++k) r2[o + k] = E.at(nt - 1, k);
+        }
+        V.ob1 = upload(b1);
+        V.ob2 = upload(b2);
+        V.or1 = upload(r1);
+        V.or2 = upload(r2);
+        V.oD = upload(D);
+    }
+
+    // coarsest direct factor (multigrid.cpp:112-121)
+    void setup_coarsest(Level& V) {
+        const int n = static_cast<int>(V.g.n());
+        const LevelView HL = host_view(V);
+        std::vector<int> nodes(n);
+        for (int i = 0; i < n; ++i) nodes[i] = i;
+        std::vector<double> Lall, Dall;
+        std::vector<int> fc;
+        std::vector<long> ro;
+        for (int b = 0; b < B; ++b) {
+            HostEnv E;
+            E.factor(n, assemble_coo(HL, V.g, b, nodes), {});
+            if (b == 0) {
+                fc = E.fc;
+                ro = E.ro;
+                Lall.resize((size_t)B * E.L.size());
+                Dall.resize((size_t)B * n);
+            } else if (E.fc != fc) {
+                throw PmgError(PMG_ERUNTIME, "coarsest factor: section structures differ");
+            }
+            std::copy(E.L.begin(), E.L.end(), Lall.begin() + (size_t)b * E.L.size());
+            std::copy(E.D.begin(), E.D.end(), Dall.begin() + (size_t)b * n);
+        }
+        V.env.n = n;
+        V.env.nnz = ro.back();
+        V.env.fc = upload(fc);
+        V.env.ro = upload(ro);
+        V.env.L = upload(Lall);
+        V.env.D = upload(Dall);
+    }
+
+    // interpolation weights of this level as the fine grid (interpolation.cpp:19-36)
+    void setup_weights(Level& V) {
+        const HostGrid& g = V.g;
+        std::vector<double> rwb(g.nr(), 0.0), rwa(g.nr(), 0.0), awb(g.nt(), 0.0),
+            awa(g.nt(), 0.0);
+        for (int sf = 1; sf + 1 < g.nr(); ++sf) {
+            rwb[sf] = g.h[sf] / (g.h[sf - 1] + g.h[sf]);
+            rwa[sf] = g.h[sf - 1] / (g.h[sf - 1] + g.h[sf]);
+        }
+        for (int tf = 1; tf < g.nt(); ++tf) {
+            awb[tf] = g.k[tf] / (g.k[tf - 1] + g.k[tf]);
+            awa[tf] = g.k[tf - 1] / (g.k[tf - 1] + g.k[tf]);
+        }
+        V.w.rwb = upload(rwb);
+        V.w.rwa = upload(rwa);
+        V.w.awb = upload(awb);
+        V.w.awa = upload(awa);
+    }
+
+    // ------------------------------------------------------------ cycle
+    void smooth(int l, const int* act) {
+        Level& V = lv[l];
+        for (int parity = 0; parity < 2; ++parity)
+            run(KK_CIRCLE, 1, [&] {
+                launch_circle(V.v, onfly, V.u, V.f, V.cil, V.cm, V.corner, V.of(), parity, act,
+                              stream);
+            });
+        if (V.v.len > 0)
+            for (int parity = 0; parity < 2; ++parity)
+                run(KK_RADIAL, 1, [&] {
+                    launch_radial(V.v, onfly, V.u, V.f, V.ril, V.rm, parity, act, stream);
+                });
+    }
+    void residual(int l, const int* act) {
+        Level& V = lv[l];
+        run(KK_RESIDUAL, 1, [&] {
+            launch_apply(V.v, onfly, 1, V.u, V.f, V.res, nullptr, 0, act, stream);
+        });
+    }
+    void restrict_to(int l, const int* act) {
+        Level& F = lv[l];
+        Level& C = lv[l + 1];
+        run(KK_RESTRICT, 1,
+            [&] { launch_restrict(F.v, C.v, F.w, F.res, C.f, C.u, true, act, stream); });
+    }
+    void prolong_add(int l, const int* act) {
+        Level& F = lv[l];
+        Level& C = lv[l + 1];
+        run(KK_PROLONG, 1, [&] { launch_prolong(F.v, C.v, F.w, C.u, F.u, true, act, stream); });
+    }
+    void coarse(int l, const int* act) {
+        Level& V = lv[l];
+        run(KK_COARSE, 1, [&] { launch_coarse(V.v, V.env, V.f, V.u, act, stream); });
+    }
+    // multigrid.cpp:189-220
+    void cycle(int l, int type, const int* act) {
+        const int L = static_cast<int>(lv.size());
+        if (l == L - 1) {
+            coarse(l, act);
+            return;
+        }
+        for (int i = 0; i < set.pre_smoothing; ++i) smooth(l, act);
+        residual(l, act);
+        restrict_to(l, act);
+        if (type == 0) {
+            cycle(l + 1, 0, act);
+        } else if (type == 1) {
+            cycle(l + 1, 1, act);
+            cycle(l + 1, 1, act);
+        } else {
+            cycle(l + 1, 2, act);
+            cycle(l + 1, 0, act);
+        }
+        prolong_add(l, act);
+        for (int i = 0; i < set.post_smoothing; ++i) smooth(l, act);
+    }
+
+    // residual norm + convergence bookkeeping of iteration `it`
+    void norm_check(int it) {
+        Level& V = lv[0];
+        int nb = 0;
+        run(KK_RESIDUAL, 1, [&] {
+            nb = launch_apply(V.v, onfly, 1, V.u, V.f, V.res, partials, set.norm_type, active,
+                              stream);
+        });
+        run(KK_NORM, 2, [&] {
+            launch_norm_final(partials, nb, B, V.v.n, set.norm_type, norms, stream);
+            ConvState cs{r0, hist, active, iters, conv, remaining, hist_cap};
+            launch_check(norms, cs, B, it, set.max_iterations, set.relative_tolerance,
+                         set.absolute_tolerance, stream);
+        });
+    }
+
+    int solve(pmg_report* reports, double* history, int history_cap) {
+        PMG_CUDA(cudaSetDevice(device));
+        cudaEvent_t e0, e1;
+        PMG_CUDA(cudaEventCreate(&e0));
+        PMG_CUDA(cudaEventCreate(&e1));
+        PMG_CUDA(cudaEventRecord(e0, stream));
+        Level& V = lv[0];
+        run(KK_OTHER, 2, [&] {
+            launch_set_active(active, remaining, B, stream);
+            launch_fill(V.u, (long)B * V.v.n, 0.0, stream);  // u = 0; Dirichlet values 0
+        });
+        PMG_CUDA(cudaMemsetAsync(conv, 0, sizeof(int) * B, stream));
+        norm_check(0);
+        int it = 0;
+        for (;;) {
+            PMG_CUDA(cudaMemcpyAsync(h_remaining, remaining, sizeof(int), cudaMemcpyDeviceToHost,
+                                     stream));
+            PMG_CUDA(cudaStreamSynchronize(stream));
+            if (set.verbose) {
+                double r;
+                PMG_CUDA(cudaMemcpy(&r, norms, sizeof(double), cudaMemcpyDeviceToHost));
+                std::printf("cycle %3d  residual %.6e\n", it, r);
+            }
+            if (*h_remaining == 0) break;
+            cycle(0, set.cycle, active);
+            ++it;
+            norm_check(it);
+        }
+        PMG_CUDA(cudaEventRecord(e1, stream));
+        PMG_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        PMG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        PMG_CUDA(cudaGetLastError());
+        last_solve_ms = ms;
+        collect_profile();
+        // reports
+        std::vector<int> h_it(B), h_conv(B);
+        std::vector<double> h_hist((size_t)B * hist_cap);
+        PMG_CUDA(cudaMemcpy(h_it.data(), iters, sizeof(int) * B, cudaMemcpyDeviceToHost));
+        PMG_CUDA(cudaMemcpy(h_conv.data(), conv, sizeof(int) * B, cudaMemcpyDeviceToHost));
+        PMG_CUDA(cudaMemcpy(h_hist.data(), hist, sizeof(double) * h_hist.size(),
+                            cudaMemcpyDeviceToHost));
+        bool all = true;
+        for (int b = 0; b < B; ++b) {
+            const int itb = h_it[b];
+            const double* hb = h_hist.data() + (size_t)b * hist_cap;
+            if (reports) {
+                pmg_report& r = reports[b];
+                std::memset(&r, 0, sizeof r);
+                r.converged = h_conv[b];
+                r.iterations = itb;
+                r.fine_cycles_total = itb;
+                r.num_residuals = itb + 1;
+                r.initial_residual = hb[0];
+                r.final_residual = hb[itb];
+                r.reduction_factor_mean = (itb > 0 && hb[0] > 0.0 && hb[itb] > 0.0)
+                                              ? std::pow(hb[itb] / hb[0], 1.0 / itb)
+                                              : 0.0;
+                r.setup_seconds = setup_seconds;
+                r.solve_seconds = ms * 1e-3;
+                r.device_bytes = bytes;
+            }
+            if (history && history_cap > 0)
+                for (int k = 0; k < history_cap; ++k)
+                    history[(size_t)b * history_cap + k] = k <= itb ? hb[k] : 0.0;
+            all = all && h_conv[b];
+        }
+        return all ? PMG_OK : PMG_ENOTCONV;
+    }
+
+    // ------------------------------------------------------------ helpers
+    void to_node(int l, const double* in, double* out, int layout) const {
+        const HostGrid& g = lv[l].g;
+        const long n = g.n();
+        if (layout == PMG_LAYOUT_NODE) {
+            std::memcpy(out, in, sizeof(double) * n * B);
+            return;
+        }
+        for (int b = 0; b < B; ++b)
+            for (int s = 0; s < g.nr(); ++s)
+                for (int t = 0; t < g.nt(); ++t)
+                    out[(long)b * n + g.idx(s, t)] = in[(long)b * n + (long)s * g.nt() + t];
+    }
+    void from_node(int l, const double* in, double* out, int layout) const {
+        const HostGrid& g = lv[l].g;
+        const long n = g.n();
+        if (layout == PMG_LAYOUT_NODE) {
+            std::memcpy(out, in, sizeof(double) * n * B);
+            return;
+        }
+        for (int b = 0; b < B; ++b)
+            for (int s = 0; s < g.nr(); ++s)
+                for (int t = 0; t < g.nt(); ++t)
+                    out[(long)b * n + (long)s * g.nt() + t] = in[(long)b * n + g.idx(s, t)];
+    }
+    void h2d(double* d, const double* h, long count) {
+        PMG_CUDA(cudaMemcpyAsync(d, h, sizeof(double) * count, cudaMemcpyHostToDevice, stream));
+    }
+    void d2h(double* h, const double* d, long count) {
+        PMG_CUDA(cudaMemcpyAsync(h, d, sizeof(double) * count, cudaMemcpyDeviceToHost, stream));
+        PMG_CUDA(cudaStreamSynchronize(stream));
+    }
+    void check_level(int l, bool need_smoother = false) const {
+        if (l < 0 || l >= static_cast<int>(lv.size()))
+            throw PmgError(PMG_EINVAL, "level out of range");
+        if (need_smoother && l == static_cast<int>(lv.size()) - 1)
+            throw PmgError(PMG_EINVAL, "the coarsest level has no smoother");
+    }
+    void sync_check() {
+        PMG_CUDA(cudaStreamSynchronize(stream));
+        PMG_CUDA(cudaGetLastError());
+    }
+    void ensure_flush() {
+        if (!flush_buf) {
+            flush_n = (256l << 20) / 8;  // 256 MiB > 126 MB L2
+            flush_buf = alloc<double>(flush_n);
+        }
+    }
+};
+
+// ------------------------------------------------------------- validation
+// SolverConfig::validate (config.cpp:150-183) on the ABI structs
+static void validate(const pmg_geometry* g, const pmg_problem* p, const pmg_grid* gr,
+                     const pmg_settings* s) {
+    if (!g || !p || !gr || !s) throw PmgError(PMG_EINVAL, "null argument");
+    if (s->extrapolation != 0 && s->extrapolation != 1)
+        throw PmgError(PMG_EINVAL, "extrapolation=" + std::to_string(s->extrapolation) +
+                                       " is not supported by this solver (use 0 or 1)");
+    if (s->extrapolation == 1)
+        throw PmgError(PMG_EINVAL,
+                       "extrapolation=1 is not supported by the B200 solve path yet");
+    if (s->fmg) throw PmgError(PMG_EINVAL, "FMG=1 is not supported by the B200 solve path yet");
+    if (p->rmax <= 0.0) throw PmgError(PMG_EINVAL, "Rmax must be positive");
+    if (p->delta_r <= 0.0) throw PmgError(PMG_EINVAL, "delta_r must be positive");
+    if (gr->mode != 2 && (gr->R0 <= 0.0 || gr->R0 >= gr->Rmax))
+        throw PmgError(PMG_EINVAL, "R0 must lie in (0, Rmax)");
+    if (gr->mode == 1) {
+        if (gr->nr_exp < 2) throw PmgError(PMG_EINVAL, "nr_exp must be at least 2");
+        if (gr->ntheta_exp < 2) throw PmgError(PMG_EINVAL, "ntheta_exp must be at least 2");
+        if (gr->anisotropic_factor < 0)
+            throw PmgError(PMG_EINVAL, "anisotropic_factor must be >= 0");
+        if (gr->divide_by_2 < 0) throw PmgError(PMG_EINVAL, "divideBy2 must be >= 0");
+    }
+    if (s->max_levels < 0) throw PmgError(PMG_EINVAL, "maxLevels must be >= 0");
+    if (s->pre_smoothing < 0 || s->post_smoothing < 0)
+        throw PmgError(PMG_EINVAL, "preSmoothingSteps/postSmoothingSteps must be >= 0");
+    if (s->max_iterations < 0) throw PmgError(PMG_EINVAL, "maxIterations must be >= 0");
+    if (s->fmg_iterations < 1) throw PmgError(PMG_EINVAL, "FMG_iterations must be >= 1");
+    if (s->max_threads < 0) throw PmgError(PMG_EINVAL, "maxOpenMPThreads must be >= 0");
+    if (s->stencil_mode != 0 && s->stencil_mode != 1)
+        throw PmgError(PMG_EINVAL, "unknown stencilDistributionMethod (expected Take or Give)");
+    if (s->cycle < 0 || s->cycle > 2)
+        throw PmgError(PMG_EINVAL, "unknown cycle type (expected V, W, or F)");
+    if (s->norm_type < 0 || s->norm_type > 2)
+        throw PmgError(PMG_EINVAL,
+                       "unknown residualNormType (expected weighted-l2, euclidean, or infinity)");
+    if (s->boundary_mode != 0 && s->boundary_mode != 1)
+        throw PmgError(PMG_EINVAL, "unknown boundary mode");
+    if (g->kind < 0 || g->kind > 2) throw PmgError(PMG_EINVAL, "unknown geometry");
+    if (g->kind == 2 && (g->kappa_eps <= 0.0 || g->kappa_eps >= 2.0))
+        throw PmgError(PMG_EINVAL, "Czarny requires 0 < epsilon < 2");
+}
+
+}  // namespace pmg
+
+// =================================================================== C ABI
+using pmg::PmgError;
+using pmg::Solver;
+
+struct pmg_solver {
+    std::unique_ptr<Solver> s;
+};
+
+template <class F>
+static int guarded(F&& fn) {
+    try {
+        fn();
+        return PMG_OK;
+    } catch (const PmgError& e) {
+        pmg::g_err = e.what();
+        return e.code;
+    } catch (const std::invalid_argument& e) {
+        pmg::g_err = e.what();
+        return PMG_EINVAL;
+    } catch (const std::bad_alloc&) {
+        pmg::g_err = "out of host memory";
+        return PMG_ERUNTIME;
+    } catch (const std::exception& e) {
+        pmg::g_err = e.what();
+        return PMG_ERUNTIME;
+    }
+}
+
+static Solver& S(pmg_handle h) {
+    if (!h || !h->s) throw PmgError(PMG_EINVAL, "null solver handle");
+    cudaSetDevice(h->s->device);
+    return *h->s;
+}
+
+extern "C" {
+
+const char* pmg_last_error(void) { return pmg::g_err.c_str(); }
+const char* pmg_version(void) { return "polarmg_b200 0.1 (sm_100a, fp64)"; }
+
+void pmg_default_settings(pmg_settings* s) {
+    std::memset(s, 0, sizeof *s);
+    s->stencil_mode = 0;
+    s->boundary_mode = 0;
+    s->cache_profile = 1;
+    s->cache_geometry = 0;
+    s->max_levels = 0;
+    s->pre_smoothing = 1;
+    s->post_smoothing = 1;
+    s->cycle = 0;
+    s->extrapolation = 0;
+    s->fmg = 0;
+    s->fmg_iterations = 2;
+    s->fmg_cycle = 2;
+    s->norm_type = 0;
+    s->max_iterations = 150;
+    s->absolute_tolerance = -1.0;
+    s->relative_tolerance = 1e-8;
+    s->max_threads = 0;
+    s->verbose = 0;
+}
+
+int pmg_create_batch(const pmg_geometry* geom, const pmg_problem* prob, const pmg_grid* grid,
+                     const pmg_settings* settings, int n_sections, const double* alpha_scales,
+                     int device, void* stream, pmg_handle* out) {
+    return guarded([&] {
+        if (!out) throw PmgError(PMG_EINVAL, "null output handle");
+        *out = nullptr;
+        pmg::validate(geom, prob, grid, settings);
+        if (n_sections < 1) throw PmgError(PMG_EINVAL, "n_sections must be >= 1");
+        int ndev = 0;
+        PMG_CUDA(cudaGetDeviceCount(&ndev));
+        if (device < 0 || device >= ndev)
+            throw PmgError(PMG_EINVAL, "CUDA device " + std::to_string(device) + " not present");
+        PMG_CUDA(cudaSetDevice(device));
+        auto s = std::make_unique<Solver>();
+        s->device = device;
+        if (stream) {
+            s->stream = static_cast<cudaStream_t>(stream);
+        } else {
+            PMG_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+            s->own_stream = true;
+        }
+        s->geo.kind = geom->kind;
+        s->geo.ke = geom->kappa_eps;
+        s->geo.de = geom->delta_e;
+        s->geo.xi = geom->kind == 2
+                        ? 1.0 / std::sqrt(1.0 - geom->kappa_eps * geom->kappa_eps / 4.0)
+                        : 1.0;
+        s->prob = *prob;
+        s->set = *settings;
+        s->B = n_sections;
+        s->scales.assign(n_sections, 1.0);
+        // alpha_scale multiplies the per-section scale (both 1 => reference alpha)
+        for (int b = 0; b < n_sections; ++b)
+            s->scales[b] = (alpha_scales ? alpha_scales[b] : 1.0) * prob->alpha_scale;
+        s->build(*grid);
+        auto* h = new pmg_solver;
+        h->s = std::move(s);
+        *out = h;
+    });
+}
+
+int pmg_create(const pmg_geometry* geom, const pmg_problem* prob, const pmg_grid* grid,
+               const pmg_settings* settings, int device, void* stream, pmg_handle* out) {
+    return pmg_create_batch(geom, prob, grid, settings, 1, nullptr, device, stream, out);
+}
+
+int pmg_destroy(pmg_handle h) {
+    return guarded([&] { delete h; });
+}
+
+int pmg_num_levels(pmg_handle h, int* levels) {
+    return guarded([&] { *levels = static_cast<int>(S(h).lv.size()); });
+}
+int pmg_num_sections(pmg_handle h, int* sections) {
+    return guarded([&] { *sections = S(h).B; });
+}
+int pmg_level_info(pmg_handle h, int level, int* n_r, int* n_theta, int* split) {
+    return guarded([&] {
+        Solver& s = S(h);
+        s.check_level(level);
+        const auto& g = s.lv[level].g;
+        *n_r = g.nr();
+        *n_theta = g.nt();
+        *split = g.split;
+    });
+}
+int pmg_level_grid(pmg_handle h, int level, double* radii, double* angles) {
+    return guarded([&] {
+        Solver& s = S(h);
+        s.check_level(level);
+        const auto& g = s.lv[level].g;
+        std::copy(g.r.begin(), g.r.end(), radii);
+        std::copy(g.th.begin(), g.th.end(), angles);
+    });
+}
+
+int pmg_set_rhs(pmg_handle h, const double* f_host, int layout) {
+    return guarded([&] {
+        Solver& s = S(h);
+        const long N = (long)s.B * s.lv[0].v.n;
+        std::vector<double> tmp(N);
+        s.to_node(0, f_host, tmp.data(), layout);
+        s.h2d(s.lv[0].f, tmp.data(), N);
+        s.sync_check();
+    });
+}
+
+int pmg_set_rhs_device(pmg_handle h, const void* f_device) {
+    return guarded([&] {
+        Solver& s = S(h);
+        const long N = (long)s.B * s.lv[0].v.n;
+        PMG_CUDA(cudaMemcpyAsync(s.lv[0].f, f_device, sizeof(double) * N,
+                                 cudaMemcpyDeviceToDevice, s.stream));
+    });
+}
+
+int pmg_seeded_rhs(pmg_handle h, unsigned seed, double* ustar_host, int layout) {
+    return guarded([&] {
+        Solver& s = S(h);
+        pmg::Level& V = s.lv[0];
+        const auto& g = V.g;
+        const long n = g.n();
+        std::vector<double> us((size_t)s.B * n);
+        for (int b = 0; b < s.B; ++b) {
+            std::mt19937 rng(seed + static_cast<unsigned>(b));
+            std::uniform_real_distribution<double> dist(-1.0, 1.0);
+            double* ub = us.data() + (size_t)b * n;
+            for (int si = 0; si < g.nr(); ++si)
+                for (int t = 0; t < g.nt(); ++t) ub[g.idx(si, t)] = dist(rng);
+            for (int t = 0; t < g.nt(); ++t) ub[g.idx(g.nr() - 1, t)] = 0.0;
+        }
+        s.h2d(V.res, us.data(), (long)us.size());
+        s.run(pmg::KK_RESIDUAL, 1, [&] {
+            pmg::launch_apply(V.v, s.onfly, 0, V.res, nullptr, V.f, nullptr, 0, nullptr,
+                              s.stream);
+        });
+        s.sync_check();
+        if (ustar_host) s.from_node(0, us.data(), ustar_host, layout);
+    });
+}
+
+int pmg_solve(pmg_handle h, pmg_report* reports, double* history, int history_cap) {
+    int rc = PMG_OK;
+    const int g = guarded([&] { rc = S(h).solve(reports, history, history_cap); });
+    if (g != PMG_OK) return g;
+    if (rc == PMG_ENOTCONV) pmg::g_err = "solve ended without meeting a tolerance";
+    return rc;
+}
+
+int pmg_get_solution(pmg_handle h, double* u_host, int layout) {
+    return guarded([&] {
+        Solver& s = S(h);
+        const long N = (long)s.B * s.lv[0].v.n;
+        std::vector<double> tmp(N);
+        s.d2h(tmp.data(), s.lv[0].u, N);
+        s.from_node(0, tmp.data(), u_host, layout);
+    });
+}
+
+int pmg_solution_device(pmg_handle h, const void** u_device) {
+    return guarded([&] { *u_device = S(h).lv[0].u; });
+}
+
+// ---- operator seams on host buffers
+int pmg_apply(pmg_handle h, int level, const double* u, double* y) {
+    return guarded([&] {
+        Solver& s = S(h);
+        s.check_level(level);
+        pmg::Level& V = s.lv[level];
+        const long N = (long)s.B * V.v.n;
+        s.h2d(V.u, u, N);
+        s.run(pmg::KK_RESIDUAL, 1, [&] {
+            pmg::launch_apply(V.v, s.onfly, 0, V.u, nullptr, V.res, nullptr, 0, nullptr,
+                              s.stream);
+        });
+        s.d2h(y, V.res, N);
+        s.sync_check();
+    });
+}
+
+int pmg_residual(pmg_handle h, int level, const double* u, const double* f, double* r) {
+    return guarded([&] {
+        Solver& s = S(h);
+        s.check_level(level);
+        pmg::Level& V = s.lv[level];
+        const long N = (long)s.B * V.v.n;
+        s.h2d(V.u, u, N);
+        s.h2d(V.f, f, N);
+        s.residual(level, nullptr);
+        s.d2h(r, V.res, N);
+        s.sync_check();
+    });
+}
+
+int pmg_smooth(pmg_handle h, int level, double* u, const double* f) {
+    return guarded([&] {
+        Solver& s = S(h);
+        s.check_level(level, true);
+        pmg::Level& V = s.lv[level];
+        const long N = (long)s.B * V.v.n;
+        s.h2d(V.u, u, N);
+        s.h2d(V.f, f, N);
+        s.smooth(level, nullptr);
+        s.d2h(u, V.u, N);
+        s.sync_check();
+    });
+}
+
+int pmg_sweep(pmg_handle h, int level, int kind, int parity, double* u, const double* f) {
+    return guarded([&] {
+        Solver& s = S(h);
+        s.check_level(level, true);
+        if (parity != 0 && parity != 1) throw PmgError(PMG_EINVAL, "parity must be 0 or 1");
+        pmg::Level& V = s.lv[level];
+        const long N = (long)s.B * V.v.n;
+        s.h2d(V.u, u, N);
+        s.h2d(V.f, f, N);
+        if (kind == 0)
+            s.run(pmg::KK_CIRCLE, 1, [&] {
+                pmg::launch_circle(V.v, s.onfly, V.u, V.f, V.cil, V.cm, V.corner, V.of(), parity,
+                                   nullptr, s.stream);
+            });
+        else if (V.v.len > 0)
+            s.run(pmg::KK_RADIAL, 1, [&] {
+                pmg::launch_radial(V.v, s.onfly, V.u, V.f, V.ril, V.rm, parity, nullptr,
+                                   s.stream);
+            });
+        s.d2h(u, V.u, N);
+        s.sync_check();
+    });
+}
+
+int pmg_restrict(pmg_handle h, int level, const double* fine, double* coarse) {
+    return guarded([&] {
+        Solver& s = S(h);
+        s.check_level(level, true);
+        pmg::Level& F = s.lv[level];
+        pmg::Level& C = s.lv[level + 1];
+        s.h2d(F.res, fine, (long)s.B * F.v.n);
+        // plain restrict_transpose: no Dirichlet masking at this seam
+        s.run(pmg::KK_RESTRICT, 1, [&] {
+            pmg::launch_restrict(F.v, C.v, F.w, F.res, C.f, nullptr, false, nullptr, s.stream);
+        });
+        s.d2h(coarse, C.f, (long)s.B * C.v.n);
+        s.sync_check();
+    });
+}
+
+int pmg_prolongate(pmg_handle h, int level, const double* coarse, double* fine, int add) {
+    return guarded([&] {
+        Solver& s = S(h);
+        s.check_level(level, true);
+        pmg::Level& F = s.lv[level];
+        pmg::Level& C = s.lv[level + 1];
+        s.h2d(C.u, coarse, (long)s.B * C.v.n);
+        if (add) s.h2d(F.u, fine, (long)s.B * F.v.n);
+        s.run(pmg::KK_PROLONG, 1, [&] {
+            pmg::launch_prolong(F.v, C.v, F.w, C.u, F.u, add != 0, nullptr, s.stream);
+        });
+        s.d2h(fine, F.u, (long)s.B * F.v.n);
+        s.sync_check();
+    });
+}
+
+int pmg_coarse_solve(pmg_handle h, const double* f, double* u) {
+    return guarded([&] {
+        Solver& s = S(h);
+        const int l = static_cast<int>(s.lv.size()) - 1;
+        pmg::Level& V = s.lv[l];
+        s.h2d(V.f, f, (long)s.B * V.v.n);
+        s.coarse(l, nullptr);
+        s.d2h(u, V.u, (long)s.B * V.v.n);
+        s.sync_check();
+    });
+}
+
+int pmg_norm(pmg_handle h, int type, const double* v_host, long n, double* out) {
+    return guarded([&] {
+        Solver& s = S(h);
+        if (type < 0 || type > 2) throw PmgError(PMG_EINVAL, "unknown norm type");
+        double* buf = s.alloc<double>(n, false);
+        double* part = s.alloc<double>(1024, false);
+        double* res = s.alloc<double>(1, false);
+        s.h2d(buf, v_host, n);
+        const int nb = pmg::launch_norm_partials(buf, n, 1, type, part, s.stream);
+        pmg::launch_norm_final(part, nb, 1, n, type, res, s.stream);
+        s.d2h(out, res, 1);
+        s.release(buf);
+        s.release(part);
+        s.release(res);
+        s.sync_check();
+    });
+}
+
+int pmg_launch_count(pmg_handle h, long long* count) {
+    return guarded([&] { *count = S(h).launches; });
+}
+
+int pmg_time_kernel(pmg_handle h, int kind, int level, int reps, int flush_l2,
+                    double* ms_per_call) {
+    return guarded([&] {
+        Solver& s = S(h);
+        s.check_level(level, kind != 0);
+        if (reps < 1) throw PmgError(PMG_EINVAL, "reps must be >= 1");
+        if (flush_l2) s.ensure_flush();
+        cudaEvent_t a, b;
+        PMG_CUDA(cudaEventCreate(&a));
+        PMG_CUDA(cudaEventCreate(&b));
+        double total = 0.0;
+        for (int r = 0; r < reps; ++r) {
+            if (flush_l2) pmg::launch_flush(s.flush_buf, s.flush_n, s.stream);
+            PMG_CUDA(cudaEventRecord(a, s.stream));
+            pmg::Level& V = s.lv[level];
+            switch (kind) {
+                case 0: s.residual(level, nullptr); break;
+                case 1:
+                    for (int p = 0; p < 2; ++p)
+                        s.run(pmg::KK_CIRCLE, 1, [&] {
+                            pmg::launch_circle(V.v, s.onfly, V.u, V.f, V.cil, V.cm, V.corner,
+                                               V.of(), p, nullptr, s.stream);
+                        });
+                    break;
+                case 2:
+                    for (int p = 0; p < 2; ++p)
+                        s.run(pmg::KK_RADIAL, 1, [&] {
+                            pmg::launch_radial(V.v, s.onfly, V.u, V.f, V.ril, V.rm, p, nullptr,
+                                               s.stream);
+                        });
+                    break;
+                case 3: s.smooth(level, nullptr); break;
+                case 4: s.restrict_to(level, nullptr); break;
+                case 5: s.prolong_add(level, nullptr); break;
+                default: throw PmgError(PMG_EINVAL, "unknown kernel kind");
+            }
+            PMG_CUDA(cudaEventRecord(b, s.stream));
+            PMG_CUDA(cudaEventSynchronize(b));
+            float ms = 0.f;
+            PMG_CUDA(cudaEventElapsedTime(&ms, a, b));
+            total += ms;
+        }
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        PMG_CUDA(cudaGetLastError());
+        *ms_per_call = total / reps;
+    });
+}
+
+int pmg_profile_enable(pmg_handle h, int on) {
+    return guarded([&] {
+        Solver& s = S(h);
+        s.collect_profile();
+        s.prof = on != 0;
+        if (on)
+            for (int k = 0; k < pmg::KK_COUNT; ++k) {
+                s.prof_ms[k] = 0.0;
+                s.prof_n[k] = 0;
+            }
+    });
+}
+
+int pmg_profile_read(pmg_handle h, int kind, double* total_ms, long long* launches) {
+    return guarded([&] {
+        Solver& s = S(h);
+        if (kind < 0 || kind >= pmg::KK_COUNT) throw PmgError(PMG_EINVAL, "unknown kernel kind");
+        s.collect_profile();
+        *total_ms = s.prof_ms[kind];
+        *launches = s.prof_n[kind];
+    });
+}
+
+}  // extern "C"
