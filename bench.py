@@ -1,0 +1,463 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 multigrid solve path (driver contract: one JSON line).
+
+Metric (BASELINE.json): multigrid DOF*V-cycles/s to a relative residual of
+1e-10, plus smoother/residual HBM GB/s.  A *step* is one full solve
+(MultigridSolver::solve, u0 = 0 .. converged norm) of the workload:
+
+  c1 (default)  Shafranov 1025x1024, Take, V(1,1)           (BASELINE configs[1])
+  c0            CirclePolar 257x256, Give, V(1,1)
+  c2v / c2w     Czarny 4097x4096, Take, V(1,1) / W(1,1)
+  c3            256 Shafranov 513x512 sections, alpha scaled per section,
+                sharded over the ranks (strong scaling, no collectives)
+  c4            Czarny 8193x8192 kernel roofline microbench (Take residual,
+                circle sweep B+W, radial sweep B+W; 100 reps each)
+
+value: device time (CUDA events on the solver's stream, L2 flushed between
+steps by a 512 MiB write) with the RHS already in HBM; e2e: the same solve
+through the public C ABI from pinned host buffers (H2D of f and D2H of u inside
+the timed region).  Multi-GPU: one process per GPU (torchrun), barrier +
+synchronize around the timed region, max over ranks.
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref, all host threads) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEED = 20240611
+METRIC = "multigrid DOF*V-cycles/sec to rel. residual 1e-10"
+UNIT = "DOF*cycles/s"
+
+WORKLOADS = {
+    "c0": (0, "CirclePolar 257x256 Give V(1,1) rel 1e-10"),
+    "c1": (1, "Shafranov 1025x1024 Take V(1,1) rel 1e-10"),
+    "c2v": (2, "Czarny 4097x4096 Take V(1,1) rel 1e-10"),
+    "c2w": (2, "Czarny 4097x4096 Take W(1,1) rel 1e-10"),
+    "c3": (3, "256 x Shafranov 513x512 Take V(1,1) rel 1e-10, alpha*U(0.5,2)"),
+    "c4": (4, "Czarny 8193x8192 Take kernel microbench"),
+}
+
+# algorithmic bytes per node of one launch
+BYTES_PER_NODE = {"residual": 56.0, "circle": 56.0, "radial": 56.0, "restrict": 10.0,
+                  "prolongate": 18.0}
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sms, mx, reasons, loaded = [], None, set(), []
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm, smmax, util = float(parts[0]), float(parts[1]), float(parts[6])
+            except ValueError:
+                continue
+            sms.append(sm)
+            mx = smmax
+            if util > 0:
+                loaded.append(sm)
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        pool = loaded or sms
+        return {"sm_mhz": statistics.median(pool) if pool else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sms), "samples_loaded": len(loaded)}
+
+
+# ---------------------------------------------------------------- reference
+def ref_case(k: int, cycle: str = "V", **over):
+    from oracle.oracle import config_case
+    c = config_case(k, cycle=cycle, **over)
+    return c
+
+
+def cpu_reference_solves(workload: str, n_solves: int, warm: int = 1, sections=None):
+    """Times the reference polarmg solve (oracle/_ref, all host threads) on the
+    workload; returns (DOF*cycles/s, seconds, solves, sample description)."""
+    from oracle.oracle import RefSolver, section_scales as ref_scales
+    k, _ = WORKLOADS[workload]
+    cycle = "W" if workload == "c2w" else "V"
+    threads = os.cpu_count() or 1
+    units = 0.0
+    secs = 0.0
+    count = 0
+    if k == 3:
+        scales = ref_scales(256)
+        idx = sections if sections is not None else list(range(min(n_solves, 256)))
+        for j, i in enumerate(idx):
+            R = RefSolver(ref_case(3, alpha_scale=float(scales[i]), threads=threads))
+            _, f = R.seeded_rhs(SEED + i)
+            if j < warm:
+                R.solve(f)
+            out = R.solve(f)
+            units += R.n(0) * out["iterations"]
+            secs += out["seconds"]
+            count += 1
+        sample = f"{count} of 256 sections (sequential, {threads} OpenMP threads each)"
+    else:
+        R = RefSolver(ref_case(k, cycle=cycle, threads=threads))
+        _, f = R.seeded_rhs(SEED)
+        for _ in range(warm):
+            R.solve(f)
+        for _ in range(n_solves):
+            out = R.solve(f)
+            units += R.n(0) * out["iterations"]
+            secs += out["seconds"]
+            count += 1
+        sample = f"{count} full solves of {WORKLOADS[workload][1]} after {warm} warm-up"
+    return units / secs, secs, count, sample, threads
+
+
+def run_reference_arm(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    wl = args.workload
+    if wl == "c4":
+        print(json.dumps({"impl": "reference", "unavailable": "c4 is a kernel microbench; use c1"}))
+        return 0
+    per_step = []
+    units_total = 0.0
+    n_per_step = 1 if wl != "c3" else 4
+    for step in range(args.warmup + args.steps):
+        secs_list = (list(range(step * n_per_step, (step + 1) * n_per_step))
+                     if wl == "c3" else None)
+        v, secs, cnt, sample, threads = cpu_reference_solves(
+            wl, n_per_step, warm=0 if step else 1, sections=secs_list)
+        if step >= args.warmup:
+            per_step.append(secs)
+            units_total += v * secs
+    total = sum(per_step)
+    value = units_total / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak" if wl != "c3" else "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded U(-1,1) u*, f = A u*)",
+        "config": {"workload": f"{wl}: {WORKLOADS[wl][1]}", "host_threads": threads},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{args.steps} steps; each step {sample}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# --------------------------------------------------------------------- GPU
+def build_solver(workload, rank, world, stream):
+    import paper_2507_03812_b200 as pmg
+    k, _ = WORKLOADS[workload]
+    cyc = "W" if workload == "c2w" else "V"
+    geom, prob, grid, st, meta = pmg.baseline_config(k, cycle=cyc)
+    sections = None
+    if k == 3:
+        scales = pmg.section_scales(256)
+        per = 256 // world
+        sections = list(range(rank * per, (rank + 1) * per))
+        solver = pmg.MultigridSolver(geom, prob, grid, st, n_sections=per,
+                                     alpha_scales=scales[sections], stream=stream)
+    else:
+        solver = pmg.MultigridSolver(geom, prob, grid, st, stream=stream)
+    return solver, sections
+
+
+def seeded(solver, workload, rank, sections):
+    if sections is not None:
+        # per-section seeds SEED + global index: seed the batch at its first index
+        solver.seeded_rhs(SEED + sections[0])
+    else:
+        solver.seeded_rhs(SEED + rank)
+
+
+def run_gpu(args):
+    import torch
+    rank, world, local = env_rank()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    peak, peak_kind = peaks()
+
+    if args.workload == "c4":
+        return run_c4(args, rank, world, local, stream, peak, peak_kind, dist)
+
+    solver, sections = build_solver(args.workload, rank, world, stream.cuda_stream)
+    seeded(solver, args.workload, rank, sections)
+    n = solver.n(0)
+    B = solver.n_sections
+    flush = torch.empty(64 << 20, dtype=torch.float64, device=dev)  # 512 MiB > 126 MB L2
+
+    def one_solve():
+        rep = solver.solve()
+        its = [r.iterations for r in solver.reports]
+        return rep, its
+
+    for _ in range(args.warmup):
+        flush.add_(1.0)
+        one_solve()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = solver.launch_count()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    units = 0.0
+    iters = None
+    for i in range(args.steps):
+        flush.add_(1.0)
+        starts[i].record(stream)
+        rep, its = one_solve()
+        ends[i].record(stream)
+        units += float(n) * sum(its)
+        iters = its
+    torch.cuda.synchronize()
+    launches = solver.launch_count() - l0
+    clk = clocks.stop()
+    dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+    if dist:
+        t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms = float(t.item())
+        u = torch.tensor([units], dtype=torch.float64, device=dev)
+        dist.all_reduce(u, op=dist.ReduceOp.SUM)
+        units = float(u.item())
+    value = units / (dev_ms * 1e-3)
+
+    # ---- e2e: public API from pinned host buffers (H2D f, solve, D2H u)
+    import ctypes
+    f_host = torch.empty(B * n, dtype=torch.float64, pin_memory=True)
+    u_host = torch.empty(B * n, dtype=torch.float64, pin_memory=True)
+    f_host.numpy()[:] = solver.get_rhs()
+    fptr = ctypes.cast(f_host.data_ptr(), ctypes.POINTER(ctypes.c_double))
+    uptr = ctypes.cast(u_host.data_ptr(), ctypes.POINTER(ctypes.c_double))
+    e2e_steps = max(3, min(args.steps, 10))
+    e2e_units = 0.0
+    e2e_total = 0.0
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    for _ in range(e2e_steps):
+        flush.add_(1.0)
+        torch.cuda.synchronize()
+        a = time.perf_counter()
+        rc1 = solver._lib.pmg_set_rhs(solver._h, fptr, 0)
+        rep, its = one_solve()
+        rc2 = solver._lib.pmg_get_solution(solver._h, uptr, 0)
+        e2e_total += time.perf_counter() - a
+        assert rc1 == 0 and rc2 == 0
+        e2e_units += float(n) * sum(its)
+    if dist:
+        t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+        u = torch.tensor([e2e_units], dtype=torch.float64, device=dev)
+        dist.all_reduce(u, op=dist.ReduceOp.SUM)
+        e2e_units = float(u.item())
+    e2e_value = e2e_units / e2e_total
+
+    # ---- per-kernel-class breakdown of one solve (CUDA events per launch)
+    solver.profile(True)
+    flush.add_(1.0)
+    one_solve()
+    breakdown = {}
+    for kind in ("residual", "circle", "radial", "restrict", "prolongate", "coarse", "norm",
+                 "other"):
+        ms, cnt = solver.profile_read(kind)
+        if cnt:
+            breakdown[kind] = {"ms": round(ms, 4), "launches": cnt}
+    solver.profile(False)
+    dominant = max(("residual", "circle", "radial"),
+                   key=lambda k: breakdown.get(k, {"ms": 0})["ms"])
+
+    # ---- roofline of the dominant kernel on the finest level
+    roof = kernel_roofline(solver, dominant, peak, peak_kind, reps=20)
+    kernels = {k: kernel_roofline(solver, k, peak, peak_kind, reps=20)
+               for k in ("residual", "circle", "radial")}
+
+    if rank != 0:
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            ns = 2 if args.workload in ("c1", "c0") else 1
+            if args.workload == "c3":
+                v, secs, cnt, sample, thr = cpu_reference_solves("c3", 8)
+            else:
+                v, secs, cnt, sample, thr = cpu_reference_solves(args.workload, ns)
+            cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "reference",
+                   "sample": sample + f" ({secs:.1f} s of CPU solve time)"}
+        except Exception as e:  # the checker must not mask a GPU result
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+    nr, nt, split = solver.level_shape(0)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if args.workload == "c3" else "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded U(-1,1) u*, f = A u*; random-free grid)",
+        "config": {"workload": f"{args.workload}: {WORKLOADS[args.workload][1]}",
+                   "grid": f"{nr}x{nt}", "split": split, "levels": solver.num_levels(),
+                   "sections_per_rank": B, "iterations": iters[:4] if iters else None,
+                   "l2": "flushed between steps (512 MiB write, untimed)",
+                   "parallelism": f"{world} independent ranks, no collectives"},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * B * n,
+                "d2h_bytes_per_step": 8 * B * n, "steps": e2e_steps,
+                "timer": "host wall clock around set_rhs + solve + get_solution"},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "breakdown_one_solve": breakdown,
+        "kernels_finest_level": kernels,
+    }
+    print(json.dumps(line))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def kernel_roofline(solver, kind, peak, peak_kind, reps=20):
+    """achieved = algorithmic bytes per launch / CUDA-event time per launch on
+    the finest level (L2 flushed before every repetition)."""
+    nr, nt, split = solver.level_shape(0)
+    B = solver.n_sections
+    if kind == "residual":
+        nodes = nr * nt
+    elif kind == "circle":
+        nodes = split * nt
+    else:
+        nodes = (nr - split) * nt
+    if nodes == 0:
+        return None
+    ms = solver.time_kernel(kind, 0, reps, True)
+    algo = BYTES_PER_NODE[kind] * nodes * B
+    gbs = algo / (ms * 1e-3) / 1e9
+    return {"kernel": f"{kind} (finest level{', B+W' if kind != 'residual' else ''})",
+            "bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(gbs / peak, 4), "traffic": None, "ms_per_launch": round(ms, 5),
+            "algorithmic_bytes": algo, "bytes_per_node": BYTES_PER_NODE[kind],
+            "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"}
+
+
+def run_c4(args, rank, world, local, stream, peak, peak_kind, dist):
+    """Config 4 roofline microbench: 100 reps of the Take residual, circle
+    sweep B+W and radial sweep B+W on seeded U(-1,1) iterates."""
+    import paper_2507_03812_b200 as pmg
+    geom, prob, grid, st, meta = pmg.baseline_config(4)
+    solver = pmg.MultigridSolver(geom, prob, grid, st, stream=stream.cuda_stream)
+    n = solver.n(0)
+    rng = np.random.default_rng(SEED)
+    # u, f ~ U(-1,1): load through the operator seams' buffers
+    u = rng.uniform(-1, 1, n)
+    f = rng.uniform(-1, 1, n)
+    solver.residual(u, f, 0)  # uploads u, f into level-0 buffers
+    reps = args.reps
+    out = {}
+    for k in ("residual", "circle", "radial"):
+        out[k] = kernel_roofline(solver, k, peak, peak_kind, reps=reps)
+    if rank == 0:
+        line = {"metric": "smoother/residual HBM GB/s (config 4 microbench)",
+                "value": out["radial"]["achieved"], "unit": "GB/s", "n_gpus": world,
+                "steps": reps, "warmup": 0, "higher_is_better": True, "dtype": "f64",
+                "config": {"workload": "c4: " + WORKLOADS["c4"][1], "grid": "8193x8192",
+                           "l2": "flushed before every repetition"},
+                "kernels": out}
+        print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
+    ap.add_argument("--workload", default="c1", choices=list(WORKLOADS))
+    ap.add_argument("--reps", type=int, default=100)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "gpu":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

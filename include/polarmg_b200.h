@@ -143,6 +143,8 @@ int pmg_level_grid(pmg_handle h, int level, double* radii, double* angles);
  * manufactured RHS in solve(), multigrid.cpp:306-317).  f_host holds
  * n_sections * n_r * n_theta doubles in `layout`. */
 int pmg_set_rhs(pmg_handle h, const double* f_host, int layout);
+/* copy of the current finest-level RHS (all sections) */
+int pmg_get_rhs(pmg_handle h, double* f_host, int layout);
 /* same from device memory (already in NODE layout) */
 int pmg_set_rhs_device(pmg_handle h, const void* f_device);
 /* seeded synthetic RHS: u* ~ U(-1,1) from std::mt19937(seed + section),

@@ -937,10 +937,24 @@ int pmg_set_rhs(pmg_handle h, const double* f_host, int layout) {
     return guarded([&] {
         Solver& s = S(h);
         const long N = (long)s.B * s.lv[0].v.n;
-        std::vector<double> tmp(N);
-        s.to_node(0, f_host, tmp.data(), layout);
-        s.h2d(s.lv[0].f, tmp.data(), N);
+        if (layout == PMG_LAYOUT_NODE) {  // device layout: one direct copy
+            s.h2d(s.lv[0].f, f_host, N);
+        } else {
+            std::vector<double> tmp(N);
+            s.to_node(0, f_host, tmp.data(), layout);
+            s.h2d(s.lv[0].f, tmp.data(), N);
+        }
         s.sync_check();
+    });
+}
+
+int pmg_get_rhs(pmg_handle h, double* f_host, int layout) {
+    return guarded([&] {
+        Solver& s = S(h);
+        const long N = (long)s.B * s.lv[0].v.n;
+        std::vector<double> tmp(N);
+        s.d2h(tmp.data(), s.lv[0].f, N);
+        s.from_node(0, tmp.data(), f_host, layout);
     });
 }
 
@@ -990,6 +1004,10 @@ int pmg_get_solution(pmg_handle h, double* u_host, int layout) {
     return guarded([&] {
         Solver& s = S(h);
         const long N = (long)s.B * s.lv[0].v.n;
+        if (layout == PMG_LAYOUT_NODE) {
+            s.d2h(u_host, s.lv[0].u, N);
+            return;
+        }
         std::vector<double> tmp(N);
         s.d2h(tmp.data(), s.lv[0].u, N);
         s.from_node(0, tmp.data(), u_host, layout);

@@ -85,7 +85,7 @@ _lib = None
 EXPORTED = [
     "pmg_last_error", "pmg_version", "pmg_default_settings", "pmg_create", "pmg_create_batch",
     "pmg_destroy", "pmg_num_levels", "pmg_num_sections", "pmg_level_info", "pmg_level_grid",
-    "pmg_set_rhs", "pmg_set_rhs_device", "pmg_seeded_rhs", "pmg_solve", "pmg_get_solution",
+    "pmg_set_rhs", "pmg_get_rhs", "pmg_set_rhs_device", "pmg_seeded_rhs", "pmg_solve", "pmg_get_solution",
     "pmg_solution_device", "pmg_apply", "pmg_residual", "pmg_smooth", "pmg_sweep",
     "pmg_restrict", "pmg_prolongate", "pmg_coarse_solve", "pmg_norm", "pmg_launch_count",
     "pmg_time_kernel", "pmg_profile_enable", "pmg_profile_read",
@@ -121,6 +121,7 @@ def load_library(path: str = LIB_PATH):
     lib.pmg_level_grid.argtypes = [vp, C.c_int, _dp, _dp]
     lib.pmg_set_rhs.argtypes = [vp, _dp, C.c_int]
     lib.pmg_set_rhs_device.argtypes = [vp, vp]
+    lib.pmg_get_rhs.argtypes = [vp, _dp, C.c_int]
     lib.pmg_seeded_rhs.argtypes = [vp, C.c_uint, _dp, C.c_int]
     lib.pmg_solve.argtypes = [vp, C.POINTER(_Report), _dp, C.c_int]
     lib.pmg_get_solution.argtypes = [vp, _dp, C.c_int]
@@ -356,6 +357,11 @@ class MultigridSolver:
         if f.size != self.n_sections * self.n(0):
             raise ValueError("rhs has the wrong size")
         _check(self._lib.pmg_set_rhs(self._h, _p(f), layout))
+
+    def get_rhs(self, layout: int = LAYOUT_NODE) -> np.ndarray:
+        f = np.zeros(self.n_sections * self.n(0))
+        _check(self._lib.pmg_get_rhs(self._h, _p(f), layout))
+        return f
 
     def set_rhs_device(self, ptr: int):
         _check(self._lib.pmg_set_rhs_device(self._h, C.c_void_p(ptr)))
