@@ -102,6 +102,11 @@ typedef struct {
     double relative_tolerance;  /* <= 0 disables */
     int max_threads;       /* accepted for API compatibility (host threads unused) */
     int verbose;
+    /* extension: 1 = every line solve in the reference's sequential operation
+     * order, making solves bitwise identical to the reference CPU solver
+     * (slower); 0 = chunked parallel line scans (default; the ill-conditioned
+     * across-origin ring always keeps the reference order). */
+    int reference_order;
 } pmg_settings;
 
 /* ConvergenceReport -- multigrid.hpp:55-68 (per section for batches) */

@@ -19,6 +19,12 @@ namespace pmg {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
+// The across-origin ring is solved with the reference's exact substitution
+// order (see origin_solve_exact); the 2x2-map scan version (origin_solve) is
+// kept for rings above this length when PMG_ORIGIN_SCAN_MIN is defined.
+#ifndef PMG_ORIGIN_SCAN_MIN
+#define PMG_ORIGIN_SCAN_MIN (1 << 30)
+#endif
 
 __device__ __forceinline__ int P(int i) { return i + (i >> 4); }  // bank-conflict padding
 __host__ __device__ __forceinline__ int padded(int n) { return n + (n >> 4) + 1; }
@@ -215,6 +221,312 @@ __device__ __forceinline__ void line_solve(double* Y, const double* IL, const do
     __syncthreads();
 }
 
+// Scan of affine maps on 2-vectors, v_out = M v_in + c (M 2x2 row-major),
+// over the threads of a block in thread order (FWD) or reverse order; returns
+// the state entering each thread's chunk (earlier maps applied to v = 0).
+struct Map2 {
+    double m00, m01, m10, m11, c0, c1;
+};
+__device__ __forceinline__ Map2 compose2(const Map2& l, const Map2& e) {  // l after e
+    Map2 r;
+    r.m00 = l.m00 * e.m00 + l.m01 * e.m10;
+    r.m01 = l.m00 * e.m01 + l.m01 * e.m11;
+    r.m10 = l.m10 * e.m00 + l.m11 * e.m10;
+    r.m11 = l.m10 * e.m01 + l.m11 * e.m11;
+    r.c0 = l.m00 * e.c0 + l.m01 * e.c1 + l.c0;
+    r.c1 = l.m10 * e.c0 + l.m11 * e.c1 + l.c1;
+    return r;
+}
+__device__ __forceinline__ Map2 shfl2(const Map2& a, int d, bool up) {
+    Map2 r;
+    r.m00 = up ? __shfl_up_sync(FULL, a.m00, d) : __shfl_down_sync(FULL, a.m00, d);
+    r.m01 = up ? __shfl_up_sync(FULL, a.m01, d) : __shfl_down_sync(FULL, a.m01, d);
+    r.m10 = up ? __shfl_up_sync(FULL, a.m10, d) : __shfl_down_sync(FULL, a.m10, d);
+    r.m11 = up ? __shfl_up_sync(FULL, a.m11, d) : __shfl_down_sync(FULL, a.m11, d);
+    r.c0 = up ? __shfl_up_sync(FULL, a.c0, d) : __shfl_down_sync(FULL, a.c0, d);
+    r.c1 = up ? __shfl_up_sync(FULL, a.c1, d) : __shfl_down_sync(FULL, a.c1, d);
+    return r;
+}
+template <bool FWD>
+__device__ __forceinline__ void block_scan2(Map2 a, double& in0, double& in1, double* scr) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const Map2 o = shfl2(a, d, FWD);
+        if (FWD ? (lane >= d) : (lane + d < 32)) a = compose2(a, o);
+    }
+    Map2* ws = reinterpret_cast<Map2*>(scr);
+    if (lane == (FWD ? 31 : 0)) ws[warp] = a;
+    __syncthreads();
+    if (warp == 0) {
+        const int wi = FWD ? lane : nw - 1 - lane;
+        Map2 w = {1.0, 0.0, 0.0, 1.0, 0.0, 0.0};
+        if (lane < nw) w = ws[wi];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const Map2 o = shfl2(w, d, true);
+            if (lane >= d) w = compose2(w, o);
+        }
+        if (lane < nw) ws[wi] = w;
+    }
+    __syncthreads();
+    const int pw = FWD ? warp - 1 : warp + 1;
+    double p0 = 0.0, p1 = 0.0;
+    if (pw >= 0 && pw < nw) {
+        p0 = ws[pw].c0;
+        p1 = ws[pw].c1;
+    }
+    const double f0 = a.m00 * p0 + a.m01 * p1 + a.c0;
+    const double f1 = a.m10 * p0 + a.m11 * p1 + a.c1;
+    const double q0 = FWD ? __shfl_up_sync(FULL, f0, 1) : __shfl_down_sync(FULL, f0, 1);
+    const double q1 = FWD ? __shfl_up_sync(FULL, f1, 1) : __shfl_down_sync(FULL, f1, 1);
+    const bool first = lane == (FWD ? 0 : 31);
+    in0 = first ? p0 : q0;
+    in1 = first ? p1 : q1;
+    __syncthreads();
+}
+
+__device__ __forceinline__ double block_sum(double v, double* scr) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_down_sync(FULL, v, d);
+    if (lane == 0) scr[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < nw; ++w) t += scr[w];
+    __syncthreads();
+    return t;
+}
+
+// Parallel solve of the across-origin ring with its envelope LDL^T factor in
+// antipodally interleaved order (reference line_algebra.cpp:211-255,
+// smoother.cpp:42-46): rows i < n-2 carry L(i,i-1), L(i,i-2) only, the two
+// closing rows are dense.  Forward and backward substitutions of the band
+// are 2nd-order linear recurrences, solved as chunked scans of 2x2 affine
+// maps; the dense rows are block reductions.  X: padded smem workspace.
+template <int K>
+__device__ void origin_solve(double* Y, double* X, const OriginFactor& of, int b, int n,
+                             double* scr) {
+    const long o = (long)b * n;
+    const double* b1 = of.band1 + o;
+    const double* b2 = of.band2 + o;
+    const double* r1 = of.row1 + o;
+    const double* r2 = of.row2 + o;
+    const double* D = of.D + o;
+    const int h = n / 2, nb = n - 2, T = blockDim.x;
+    const int j0 = threadIdx.x * K;
+    for (int k = threadIdx.x; k < n; k += T) X[P(k)] = Y[P((k & 1) ? h + (k >> 1) : (k >> 1))];
+    __syncthreads();
+    // forward band: z_i = x_i - L(i,i-2) z_{i-2} - L(i,i-1) z_{i-1}; state (z_{i-1}, z_i)
+    Map2 m = {1.0, 0.0, 0.0, 1.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+        const int i = j0 + q;
+        if (i < nb) {
+            const double l1 = i >= 1 ? b1[i] : 0.0, l2 = i >= 2 ? b2[i] : 0.0;
+            const Map2 mi = {0.0, 1.0, -l2, -l1, 0.0, X[P(i)]};
+            m = compose2(mi, m);
+        }
+    }
+    double zm2, zm1;
+    block_scan2<true>(m, zm2, zm1, scr);
+    double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+        const int i = j0 + q;
+        if (i < nb) {
+            double sum = X[P(i)];
+            if (i >= 2) sum -= b2[i] * zm2;
+            if (i >= 1) sum -= b1[i] * zm1;
+            X[P(i)] = sum;
+            zm2 = zm1;
+            zm1 = sum;
+            if (i >= of.fc1) s1 += r1[i] * sum;
+            if (i >= of.fc2) s2 += r2[i] * sum;
+        }
+    }
+    s1 = block_sum(s1, scr);
+    s2 = block_sum(s2, scr + 32);
+    if (threadIdx.x == 0) {  // dense closing rows, then their diagonal scaling
+        const double zn2 = X[P(n - 2)] - s1;
+        double zn1 = X[P(n - 1)] - s2;
+        if (n - 2 >= of.fc2) zn1 -= r2[n - 2] * zn2;
+        const double xn1 = zn1 / D[n - 1];
+        double xn2 = zn2 / D[n - 2];
+        if (n - 2 >= of.fc2) xn2 -= r2[n - 2] * xn1;
+        X[P(n - 1)] = xn1;
+        X[P(n - 2)] = xn2;
+    }
+    __syncthreads();
+    const double xn1 = X[P(n - 1)], xn2 = X[P(n - 2)];
+    // backward band: x_k = g_k - L(k+2,k) x_{k+2} - L(k+1,k) x_{k+1},
+    // g_k = w_k - L(n-1,k) x_{n-1} - L(n-2,k) x_{n-2}; state (x_{k+1}, x_{k+2})
+    Map2 g = {1.0, 0.0, 0.0, 1.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = K - 1; q >= 0; --q) {
+        const int k = j0 + q;
+        if (k < nb) {
+            double gk = X[P(k)] / D[k];
+            if (k >= of.fc2) gk -= r2[k] * xn1;
+            if (k >= of.fc1) gk -= r1[k] * xn2;
+            X[P(k)] = gk;
+            const double l1 = k + 1 < nb ? b1[k + 1] : 0.0;
+            const double l2 = k + 2 < nb ? b2[k + 2] : 0.0;
+            const Map2 mk = {-l1, -l2, 1.0, 0.0, gk, 0.0};
+            g = compose2(mk, g);
+        }
+    }
+    double xp1, xp2;
+    block_scan2<false>(g, xp1, xp2, scr);
+#pragma unroll
+    for (int q = K - 1; q >= 0; --q) {
+        const int k = j0 + q;
+        if (k < nb) {
+            double x = X[P(k)];
+            if (k + 2 < nb) x -= b2[k + 2] * xp2;
+            if (k + 1 < nb) x -= b1[k + 1] * xp1;
+            X[P(k)] = x;
+            xp2 = xp1;
+            xp1 = x;
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < n; k += T) Y[P((k & 1) ? h + (k >> 1) : (k >> 1))] = X[P(k)];
+    __syncthreads();
+}
+
+// Correctly rounded a / l given r = RN(1/l) (Markstein): q0 = RN(a r) is
+// within 1 ulp, e = a - l q0 is exact (FMA), RN(q0 + e r) = RN(a / l).  The
+// reciprocal is off the dependency chain, so a sequential substitution costs
+// 3 dependent FP64 ops per division instead of a full IEEE division.
+__device__ __forceinline__ double xdiv(double a, double l, double r) {
+    const double q0 = a * r;
+    const double e = fma(-l, q0, a);
+    return fma(e, r, q0);
+}
+
+// Sequential L L^T solve in the reference's exact operation order
+// (tridiag_solve, line_algebra.cpp:42-62) -- bitwise identical results.
+// Run by ONE thread on shared memory; Ld holds the raw L diagonal.
+__device__ void tri_solve_exact(double* Y, const double* Ld, const double* M, int n) {
+    double l = Ld[P(0)];
+    double y = xdiv(Y[P(0)], l, __drcp_rn(l));
+    Y[P(0)] = y;
+#pragma unroll 4
+    for (int i = 1; i < n; ++i) {
+        const double li = Ld[P(i)];
+        const double ri = __drcp_rn(li);
+        y = xdiv(Y[P(i)] - M[P(i - 1)] * y, li, ri);
+        Y[P(i)] = y;
+    }
+    l = Ld[P(n - 1)];
+    y = xdiv(y, l, __drcp_rn(l));
+    Y[P(n - 1)] = y;
+#pragma unroll 4
+    for (int i = n - 2; i >= 0; --i) {
+        const double li = Ld[P(i)];
+        const double ri = __drcp_rn(li);
+        y = xdiv(Y[P(i)] - M[P(i)] * y, li, ri);
+        Y[P(i)] = y;
+    }
+}
+
+// Cyclic (Sherman-Morrison) solve in the reference's exact order
+// (cyclic_tridiag_solve, line_algebra.cpp:98-120).  z = T^{-1}(e_1 + e_n) is
+// rhs-independent; it was computed at setup by the same exact sequence
+// (k_circle_z), so reading it equals recomputing it bit for bit.
+__device__ void cyc_solve_exact(double* Y, const double* Ld, const double* M, int n, double c,
+                                const double* __restrict__ z, double* scr) {
+    if (threadIdx.x == 0) {
+        tri_solve_exact(Y, Ld, M, n);
+        scr[0] = c * (Y[P(0)] + Y[P(n - 1)]) / (1.0 + c * (z[0] + z[n - 1]));
+    }
+    __syncthreads();
+    const double tau = scr[0];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) Y[P(i)] -= tau * z[i];
+    __syncthreads();
+}
+
+// Across-origin ring solve in the reference's exact operation order
+// (line_algebra.cpp:211-255 with the interleaved permutation of
+// smoother.cpp:42-46) -- bitwise identical to the reference.  Only the two
+// true recurrence chains (band forward / band backward) run on one thread;
+// the band factors are staged in shared memory, the diagonal scaling and the
+// dense-row column updates of the backward substitution are per element and
+// run on all threads (same per-element operation order as the reference).
+// Y: rhs in NATURAL order (padded) in, solution out.
+__device__ __forceinline__ int operm(int k, int h) { return (k & 1) ? h + (k >> 1) : (k >> 1); }
+
+__device__ void origin_solve_exact(double* Y, double* B1, double* B2, const OriginFactor& of,
+                                   int b, int n) {
+    const long o = (long)b * n;
+    const double* __restrict__ r1 = of.row1 + o;
+    const double* __restrict__ r2 = of.row2 + o;
+    const double* __restrict__ D = of.D + o;
+    const int h = n / 2, nb = n - 2, T = blockDim.x;
+    for (int i = threadIdx.x; i < n; i += T) {
+        B1[P(i)] = of.band1[o + i];
+        B2[P(i)] = of.band2[o + i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // forward: band rows, with the two dense-row sums accumulated in the
+        // reference's k order as the z_k become available
+        double zm2 = 0.0, zm1 = 0.0;
+        double s1 = Y[P(operm(n - 2, h))], s2 = Y[P(operm(n - 1, h))];
+        const int fc1 = of.fc1, fc2 = of.fc2;
+#pragma unroll 4
+        for (int i = 0; i < nb; ++i) {
+            const int pi = P(operm(i, h));
+            double sum = Y[pi];
+            if (i >= 2) sum -= B2[P(i)] * zm2;
+            if (i >= 1) sum -= B1[P(i)] * zm1;
+            Y[pi] = sum;
+            zm2 = zm1;
+            zm1 = sum;
+            if (i >= fc1) s1 -= r1[i] * sum;
+            if (i >= fc2) s2 -= r2[i] * sum;
+        }
+        if (n - 2 >= fc2) s2 -= r2[n - 2] * s1;
+        Y[P(operm(n - 2, h))] = s1;
+        Y[P(operm(n - 1, h))] = s2;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += T) Y[P(operm(i, h))] /= D[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const double xn1 = Y[P(operm(n - 1, h))];
+        if (n - 2 >= of.fc2) Y[P(operm(n - 2, h))] -= r2[n - 2] * xn1;
+    }
+    __syncthreads();
+    {
+        const double xn1 = Y[P(operm(n - 1, h))], xn2 = Y[P(operm(n - 2, h))];
+        for (int k = threadIdx.x; k < nb; k += T) {
+            double x = Y[P(operm(k, h))];
+            if (k >= of.fc2) x -= r2[k] * xn1;
+            if (k >= of.fc1) x -= r1[k] * xn2;
+            Y[P(operm(k, h))] = x;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // band backward: row i updates x_{i-2} then x_{i-1}; x_k is final once
+        // rows k+2 and k+1 have been applied
+        double xp1 = 0.0, xp2 = 0.0;  // x_{k+1}, x_{k+2}
+#pragma unroll 4
+        for (int k = nb - 1; k >= 0; --k) {
+            const int pk = P(operm(k, h));
+            double x = Y[pk];
+            if (k + 2 < nb) x -= B2[P(k + 2)] * xp2;
+            if (k + 1 < nb) x -= B1[P(k + 1)] * xp1;
+            Y[pk] = x;
+            xp2 = xp1;
+            xp1 = x;
+        }
+    }
+    __syncthreads();
+}
+
 // Serial envelope solve of the across-origin ring (reference
 // line_algebra.cpp:211-255 with permutation smoother.cpp:42-46); run by one
 // thread on the shared-memory rhs.
@@ -335,7 +647,9 @@ __global__ void __launch_bounds__(512) k_circle(LevelView L, double* __restrict_
                                                 const double* __restrict__ cil,
                                                 const double* __restrict__ cm,
                                                 const double* __restrict__ corner,
-                                                OriginFactor of, int parity,
+                                                const double* __restrict__ cz,
+                                                OriginFactor of, int parity, int serial,
+                                                int exact_rings,
                                                 const int* __restrict__ active) {
     extern __shared__ double smem[];
     const int b = blockIdx.y;
@@ -374,16 +688,22 @@ __global__ void __launch_bounds__(512) k_circle(LevelView L, double* __restrict_
     }
     if (s == 0 && L.boundary == 0) {
         __syncthreads();
-        if (threadIdx.x == 0) origin_solve_serial(Y, IL, of, b, nt);
-        __syncthreads();
+        if (nt < PMG_ORIGIN_SCAN_MIN)
+            origin_solve_exact(Y, IL, M, of, b, nt);
+        else
+            origin_solve<K>(Y, IL, of, b, nt, scr);
     } else {
         const long fo = (long)b * L.split * nt + (long)s * nt;
+        const bool exact = serial || s <= exact_rings;  // block-uniform
         for (int t = threadIdx.x; t < nt; t += T) {
-            IL[P(t)] = cil[fo + t];
+            IL[P(t)] = exact ? cil[fo + t] : 1.0 / cil[fo + t];
             M[P(t)] = cm[fo + t];
         }
         __syncthreads();
-        line_solve<K, true>(Y, IL, M, nt, corner[(long)b * L.split + s], scr);
+        if (exact)
+            cyc_solve_exact(Y, IL, M, nt, corner[(long)b * L.split + s], cz + fo, scr);
+        else
+            line_solve<K, true>(Y, IL, M, nt, corner[(long)b * L.split + s], scr);
     }
     for (int t = threadIdx.x; t < nt; t += T) U[base + t] = Y[P(t)];
 }
@@ -398,7 +718,7 @@ __global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict_
                                                 const double* __restrict__ f,
                                                 const double* __restrict__ ril,
                                                 const double* __restrict__ rm, int parity,
-                                                const int* __restrict__ active) {
+                                                int serial, const int* __restrict__ active) {
     extern __shared__ double smem[];
     const int b = blockIdx.y;
     if (active && !active[b]) return;
@@ -418,7 +738,7 @@ __global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict_
     const long fo = ((long)b * L.nt + t) * len;
     for (int i = threadIdx.x; i < len; i += T) {
         const int s = split + i;
-        IL[P(i)] = ril[fo + i];
+        IL[P(i)] = serial ? ril[fo + i] : 1.0 / ril[fo + i];
         M[P(i)] = rm[fo + i];
         if (L.dir(s)) {
             Y[P(i)] = F[base + i];
@@ -440,7 +760,12 @@ __global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict_
         Y[P(i)] = acc;
     }
     __syncthreads();
-    line_solve<K, false>(Y, IL, M, len, 0.0, scr);
+    if (serial) {
+        if (threadIdx.x == 0) tri_solve_exact(Y, IL, M, len);
+        __syncthreads();
+    } else {
+        line_solve<K, false>(Y, IL, M, len, 0.0, scr);
+    }
     for (int i = threadIdx.x; i < len; i += T) U[base + i] = Y[P(i)];
 }
 
@@ -662,7 +987,7 @@ inline void line_shape(int n, int& K, int& T) {
     if (T < 32) T = 32;
 }
 
-inline size_t line_smem(int n) { return (size_t)(3 * padded(n) + 32 * 3 + 8) * sizeof(double); }
+inline size_t line_smem(int n) { return (size_t)(3 * padded(n) + 32 * 6 + 16) * sizeof(double); }
 
 }  // namespace
 
@@ -695,24 +1020,28 @@ int launch_apply(const LevelView& L, bool onfly, int mode, const double* u, cons
 
 template <bool ON, int K>
 static void circle_k(const LevelView& L, double* u, const double* f, const double* cil,
-                     const double* cm, const double* corner, const OriginFactor& of, int parity,
+                     const double* cm, const double* corner, const double* cz,
+                     const OriginFactor& of, int parity, bool serial, int exact_rings,
                      const int* active, cudaStream_t st, int T, int lines) {
     const size_t sm = line_smem(L.nt);
     set_smem(k_circle<ON, K>, sm);
-    k_circle<ON, K><<<dim3(lines, L.B), T, sm, st>>>(L, u, f, cil, cm, corner, of, parity,
-                                                      active);
+    k_circle<ON, K><<<dim3(lines, L.B), T, sm, st>>>(L, u, f, cil, cm, corner, cz, of, parity,
+                                                      serial ? 1 : 0, exact_rings, active);
 }
 
 void launch_circle(const LevelView& L, bool onfly, double* u, const double* f, const double* cil,
-                   const double* cm, const double* corner, const OriginFactor& of, int parity,
+                   const double* cm, const double* corner, const double* cz,
+                   const OriginFactor& of, int parity, bool serial, int exact_rings,
                    const int* active, cudaStream_t st) {
     const int lines = L.split > parity ? (L.split - parity + 1) / 2 : 0;
     if (lines == 0) return;
     int K, T;
     line_shape(L.nt, K, T);
-#define PMG_C(KK)                                                                        \
-    (onfly ? circle_k<true, KK>(L, u, f, cil, cm, corner, of, parity, active, st, T, lines) \
-           : circle_k<false, KK>(L, u, f, cil, cm, corner, of, parity, active, st, T, lines))
+#define PMG_C(KK)                                                                            \
+    (onfly ? circle_k<true, KK>(L, u, f, cil, cm, corner, cz, of, parity, serial, exact_rings, \
+                                active, st, T, lines)                                      \
+           : circle_k<false, KK>(L, u, f, cil, cm, corner, cz, of, parity, serial, exact_rings, \
+                                 active, st, T, lines))
     switch (K) {
         case 2: PMG_C(2); break;
         case 4: PMG_C(4); break;
@@ -724,22 +1053,24 @@ void launch_circle(const LevelView& L, bool onfly, double* u, const double* f, c
 
 template <bool ON, int K>
 static void radial_k(const LevelView& L, double* u, const double* f, const double* ril,
-                     const double* rm, int parity, const int* active, cudaStream_t st, int T,
-                     int lines) {
+                     const double* rm, int parity, bool serial, const int* active,
+                     cudaStream_t st, int T, int lines) {
     const size_t sm = line_smem(L.len);
     set_smem(k_radial<ON, K>, sm);
-    k_radial<ON, K><<<dim3(lines, L.B), T, sm, st>>>(L, u, f, ril, rm, parity, active);
+    k_radial<ON, K><<<dim3(lines, L.B), T, sm, st>>>(L, u, f, ril, rm, parity, serial ? 1 : 0,
+                                                      active);
 }
 
 void launch_radial(const LevelView& L, bool onfly, double* u, const double* f, const double* ril,
-                   const double* rm, int parity, const int* active, cudaStream_t st) {
+                   const double* rm, int parity, bool serial, const int* active,
+                   cudaStream_t st) {
     if (L.len <= 0) return;
     const int lines = (L.nt - parity + 1) / 2;
     int K, T;
     line_shape(L.len, K, T);
-#define PMG_R(KK)                                                               \
-    (onfly ? radial_k<true, KK>(L, u, f, ril, rm, parity, active, st, T, lines) \
-           : radial_k<false, KK>(L, u, f, ril, rm, parity, active, st, T, lines))
+#define PMG_R(KK)                                                                       \
+    (onfly ? radial_k<true, KK>(L, u, f, ril, rm, parity, serial, active, st, T, lines) \
+           : radial_k<false, KK>(L, u, f, ril, rm, parity, serial, active, st, T, lines))
     switch (K) {
         case 2: PMG_R(2); break;
         case 4: PMG_R(4); break;

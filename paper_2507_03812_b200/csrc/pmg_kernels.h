@@ -58,11 +58,17 @@ int launch_apply(const LevelView& L, bool onfly, int mode, const double* u, cons
                  cudaStream_t st);
 int apply_blocks(const LevelView& L);
 
+// serial: line solves in the reference's sequential operation order (bitwise
+// reproduction of the reference); otherwise chunked parallel scans.
+// exact_rings: circle rings s <= exact_rings use the exact-order solve even
+// when serial is false (the ill-conditioned innermost rings).
 void launch_circle(const LevelView& L, bool onfly, double* u, const double* f, const double* cil,
-                   const double* cm, const double* corner, const OriginFactor& of, int parity,
+                   const double* cm, const double* corner, const double* cz,
+                   const OriginFactor& of, int parity, bool serial, int exact_rings,
                    const int* active, cudaStream_t st);
 void launch_radial(const LevelView& L, bool onfly, double* u, const double* f, const double* ril,
-                   const double* rm, int parity, const int* active, cudaStream_t st);
+                   const double* rm, int parity, bool serial, const int* active,
+                   cudaStream_t st);
 
 // mask: zero the coarse Dirichlet rows (mask_dirichlet_rows, multigrid.cpp:146-153)
 void launch_restrict(const LevelView& F, const LevelView& C, const Weights& w, const double* fr,
@@ -103,6 +109,9 @@ void launch_coeffs(const LevelView& L, double* arr, double* art, double* att, do
 // circle-line cyclic factors of rings [0, split) (ring 0 skipped when across-origin)
 void launch_factor_circle(const LevelView& L, bool onfly, double* cil, double* cm,
                           double* corner, int* bad, cudaStream_t st);
+// z = T^{-1}(e_1 + e_n) of every circle line, exact reference order
+void launch_circle_z(const LevelView& L, const double* cil, const double* cm, double* cz,
+                     cudaStream_t st);
 void launch_factor_radial(const LevelView& L, bool onfly, double* ril, double* rm, int* bad,
                           cudaStream_t st);
 // f = A u on the finest level for seeded RHS (same as launch_apply mode 0)

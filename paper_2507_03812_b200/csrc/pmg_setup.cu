@@ -62,7 +62,7 @@ __device__ void factor_circle_line(const LevelView& L, const CFT& cf, int s, dou
             m[t - 1] = mm;
             l = sqrt(piv);
         }
-        il[t] = 1.0 / l;
+        il[t] = l;  // L diagonal (the kernels divide by it or take 1/l)
         lprev = l;
         offprev = R.tp;  // A((s,t),(s,t+1)) for t < nt-1
     }
@@ -122,14 +122,51 @@ __global__ void k_factor_radial(LevelView L, double* ril, double* rm, int* bad) 
             m[i - 1] = mm;
             l = sqrt(piv);
         }
-        il[i] = 1.0 / l;
+        il[i] = l;
         lprev = l;
         offprev = R.has_sp ? R.sp : 0.0;  // A((s,t),(s+1,t)); 0 next to the Dirichlet ring
     }
     m[L.len - 1] = 0.0;
 }
 
+__device__ __forceinline__ double xdiv_s(double a, double l, double r) {
+    const double q0 = a * r;
+    const double e = fma(-l, q0, a);
+    return fma(e, r, q0);
+}
+
+// z = T^{-1}(e_1 + e_n) by the exact sequential substitution of
+// line_algebra.cpp:42-62 (same bits as the reference's per-solve recompute)
+__global__ void k_circle_z(LevelView L, const double* cl, const double* cm, double* cz) {
+    const int b = blockIdx.y;
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= L.split) return;
+    const int n = L.nt;
+    const long o = (long)b * L.split * n + (long)s * n;
+    const double* l = cl + o;
+    const double* m = cm + o;
+    double* z = cz + o;
+    double y = xdiv_s(1.0, l[0], __drcp_rn(l[0]));
+    z[0] = y;
+    for (int i = 1; i < n; ++i) {
+        y = xdiv_s((i == n - 1 ? 1.0 : 0.0) - m[i - 1] * y, l[i], __drcp_rn(l[i]));
+        z[i] = y;
+    }
+    y = xdiv_s(y, l[n - 1], __drcp_rn(l[n - 1]));
+    z[n - 1] = y;
+    for (int i = n - 2; i >= 0; --i) {
+        y = xdiv_s(z[i] - m[i] * y, l[i], __drcp_rn(l[i]));
+        z[i] = y;
+    }
+}
+
 }  // namespace
+
+void launch_circle_z(const LevelView& L, const double* cil, const double* cm, double* cz,
+                     cudaStream_t st) {
+    if (L.split <= 0) return;
+    k_circle_z<<<dim3((L.split + 63) / 64, L.B), 64, 0, st>>>(L, cil, cm, cz);
+}
 
 void launch_coeffs(const LevelView& L, double* arr, double* art, double* att, double* det,
                    int* bad, cudaStream_t st) {

@@ -8,6 +8,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -175,6 +176,7 @@ struct Level {
     double *u = nullptr, *f = nullptr, *res = nullptr;
     double *arr = nullptr, *art = nullptr, *att = nullptr, *det = nullptr;
     double *cil = nullptr, *cm = nullptr, *corner = nullptr, *ril = nullptr, *rm = nullptr;
+    double* cz = nullptr;  // Sherman-Morrison vectors of the circle lines (exact path)
     double *ob1 = nullptr, *ob2 = nullptr, *or1 = nullptr, *or2 = nullptr, *oD = nullptr;
     int ofc1 = 0, ofc2 = 0;
     Weights w{};
@@ -193,6 +195,8 @@ struct Solver {
     std::vector<double> scales;
     double tol = 1e-12;
     bool onfly = false;
+    bool serial = false;  // reference_order line solves
+    int exact_rings = 0;  // innermost circle rings solved in exact order (fast mode)
     std::vector<Level> lv;
     std::vector<void*> allocs;
     size_t bytes = 0;
@@ -311,6 +315,8 @@ struct Solver {
         const int L = static_cast<int>(grids.size());
         lv.resize(L);
         onfly = set.stencil_mode == 1 && !set.cache_geometry;
+        serial = set.reference_order != 0;
+        if (const char* e = std::getenv("PMG_EXACT_RINGS")) exact_rings = std::atoi(e);
         int* bad = alloc<int>(1);
         for (int l = 0; l < L; ++l) {
             Level& V = lv[l];
@@ -418,6 +424,8 @@ struct Solver {
             PMG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), stream));
             launch_factor_circle(v, onfly, V.cil, V.cm, V.corner, bad, stream);
             check_bad(bad, "cyclic core not positive definite after rank-one shift");
+            V.cz = alloc<double>((size_t)B * v.split * nt, false);
+            launch_circle_z(v, V.cil, V.cm, V.cz, stream);
             if (v.len > 0) {
                 V.ril = alloc<double>((size_t)B * nt * v.len, false);
                 V.rm = alloc<double>((size_t)B * nt * v.len, false);
@@ -560,13 +568,13 @@ struct Solver {
         Level& V = lv[l];
         for (int parity = 0; parity < 2; ++parity)
             run(KK_CIRCLE, 1, [&] {
-                launch_circle(V.v, onfly, V.u, V.f, V.cil, V.cm, V.corner, V.of(), parity, act,
-                              stream);
+                launch_circle(V.v, onfly, V.u, V.f, V.cil, V.cm, V.corner, V.cz, V.of(), parity,
+                              serial, exact_rings, act, stream);
             });
         if (V.v.len > 0)
             for (int parity = 0; parity < 2; ++parity)
                 run(KK_RADIAL, 1, [&] {
-                    launch_radial(V.v, onfly, V.u, V.f, V.ril, V.rm, parity, act, stream);
+                    launch_radial(V.v, onfly, V.u, V.f, V.ril, V.rm, parity, serial, act, stream);
                 });
     }
     void residual(int l, const int* act) {
@@ -1074,12 +1082,12 @@ int pmg_sweep(pmg_handle h, int level, int kind, int parity, double* u, const do
         s.h2d(V.f, f, N);
         if (kind == 0)
             s.run(pmg::KK_CIRCLE, 1, [&] {
-                pmg::launch_circle(V.v, s.onfly, V.u, V.f, V.cil, V.cm, V.corner, V.of(), parity,
-                                   nullptr, s.stream);
+                pmg::launch_circle(V.v, s.onfly, V.u, V.f, V.cil, V.cm, V.corner, V.cz, V.of(),
+                                   parity, s.serial, s.exact_rings, nullptr, s.stream);
             });
         else if (V.v.len > 0)
             s.run(pmg::KK_RADIAL, 1, [&] {
-                pmg::launch_radial(V.v, s.onfly, V.u, V.f, V.ril, V.rm, parity, nullptr,
+                pmg::launch_radial(V.v, s.onfly, V.u, V.f, V.ril, V.rm, parity, s.serial, nullptr,
                                    s.stream);
             });
         s.d2h(u, V.u, N);
@@ -1174,14 +1182,15 @@ int pmg_time_kernel(pmg_handle h, int kind, int level, int reps, int flush_l2,
                     for (int p = 0; p < 2; ++p)
                         s.run(pmg::KK_CIRCLE, 1, [&] {
                             pmg::launch_circle(V.v, s.onfly, V.u, V.f, V.cil, V.cm, V.corner,
-                                               V.of(), p, nullptr, s.stream);
+                                               V.cz, V.of(), p, s.serial, s.exact_rings,
+                                               nullptr, s.stream);
                         });
                     break;
                 case 2:
                     for (int p = 0; p < 2; ++p)
                         s.run(pmg::KK_RADIAL, 1, [&] {
-                            pmg::launch_radial(V.v, s.onfly, V.u, V.f, V.ril, V.rm, p, nullptr,
-                                               s.stream);
+                            pmg::launch_radial(V.v, s.onfly, V.u, V.f, V.ril, V.rm, p, s.serial,
+                                               nullptr, s.stream);
                         });
                     break;
                 case 3: s.smooth(level, nullptr); break;

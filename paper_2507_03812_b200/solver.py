@@ -20,7 +20,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libpolarmg_b200.so")
+LIB_PATH = os.environ.get("PMG_LIB") or os.path.join(_HERE, "lib", "libpolarmg_b200.so")
 
 PMG_OK, PMG_EINVAL, PMG_ERUNTIME, PMG_ECUDA, PMG_ENOTCONV = 0, 1, 2, 3, 4
 LAYOUT_NODE, LAYOUT_CANONICAL = 0, 1
@@ -67,7 +67,7 @@ class _Settings(C.Structure):
                 ("fmg", C.c_int), ("fmg_iterations", C.c_int), ("fmg_cycle", C.c_int),
                 ("norm_type", C.c_int), ("max_iterations", C.c_int),
                 ("absolute_tolerance", C.c_double), ("relative_tolerance", C.c_double),
-                ("max_threads", C.c_int), ("verbose", C.c_int)]
+                ("max_threads", C.c_int), ("verbose", C.c_int), ("reference_order", C.c_int)]
 
 
 class _Report(C.Structure):
@@ -237,6 +237,8 @@ class MultigridSettings:
     relative_tolerance: float = 1e-8
     max_threads: int = 0
     verbose: bool = False
+    # extension: line solves in the reference's sequential order (bitwise parity)
+    reference_order: bool = False
 
 
 @dataclass
@@ -297,7 +299,8 @@ class MultigridSolver:
                       _lookup(CYCLE, settings.fmg_cycle, "cycle type"),
                       _lookup(NORM, settings.norm_type, "residualNormType"),
                       settings.max_iterations, settings.absolute_tolerance,
-                      settings.relative_tolerance, settings.max_threads, int(settings.verbose))
+                      settings.relative_tolerance, settings.max_threads, int(settings.verbose),
+                      int(settings.reference_order))
         h = C.c_void_p()
         scales = None
         if alpha_scales is not None:

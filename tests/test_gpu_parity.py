@@ -27,7 +27,7 @@ Checker = RefSolver if have_ref() else OracleSolver
 GEO = {"CirclePolar": (0.0, 0.0), "Shafranov": (0.3, 0.2), "Czarny": (0.3, 1.4)}
 
 
-def gpu_solver(c: Case, n_sections=1, scales=None):
+def gpu_solver(c: Case, n_sections=1, scales=None, reference_order=False):
     geom = pmg.GeometryMap(c.geometry, c.kappa_eps, c.delta_e)
     prob = pmg.ProblemCase("Zoni" if c.alpha_coeff else "Poisson",
                            "InverseAlpha" if c.beta_coeff else "Zero", c.rmax, c.alpha_jump,
@@ -41,7 +41,8 @@ def gpu_solver(c: Case, n_sections=1, scales=None):
                                max_levels=c.max_levels, pre_smoothing=c.pre,
                                post_smoothing=c.post, cycle=c.cycle, norm_type=c.norm_type,
                                max_iterations=c.max_iterations,
-                               absolute_tolerance=c.abs_tol, relative_tolerance=c.rel_tol)
+                               absolute_tolerance=c.abs_tol, relative_tolerance=c.rel_tol,
+                               reference_order=reference_order)
     return pmg.MultigridSolver(geom, prob, grid, st, n_sections=n_sections, alpha_scales=scales)
 
 
@@ -66,10 +67,12 @@ def relmax(a, b):
     return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
 
 
-@pytest.fixture(scope="module", params=list(CASES))
+@pytest.fixture(scope="module", params=[(k, ro) for k in CASES for ro in (False, True)],
+                ids=lambda p: f"{p[0]}-{'reforder' if p[1] else 'fast'}")
 def pair(request):
-    c = CASES[request.param]
-    return request.param, c, Checker(c), gpu_solver(c)
+    name, ro = request.param
+    c = CASES[name]
+    return ro, c, Checker(c), gpu_solver(c, reference_order=ro)
 
 
 def test_hierarchy(pair):
@@ -115,7 +118,7 @@ def test_coarse_solve(pair):
 
 
 def test_sweeps(pair):
-    _, c, ref, gpu = pair
+    ro, c, ref, gpu = pair
     for l in range(ref.num_levels - 1):
         rng = np.random.default_rng(100 + l)
         u = rng.uniform(-1, 1, ref.n(l))
@@ -124,20 +127,34 @@ def test_sweeps(pair):
             for parity in (0, 1):
                 a = gpu.sweep(u, f, kind, parity, l)
                 b = ref.sweep(u, f, kind, parity, l)
-                assert relmax(a, b) < 1e-12, (l, kind, parity, relmax(a, b))
+                if ro and c.stencil_mode == "Take":
+                    assert np.array_equal(a, b), (l, kind, parity, relmax(a, b))
+                else:
+                    assert relmax(a, b) < 1e-12, (l, kind, parity, relmax(a, b))
         a = gpu.smooth(u, f, l)
         b = ref.smooth(u, f, l)
-        assert relmax(a, b) < 1e-12, (l, relmax(a, b))
+        if ro and c.stencil_mode == "Take":
+            assert np.array_equal(a, b), (l, relmax(a, b))
+        else:
+            assert relmax(a, b) < 1e-12, (l, relmax(a, b))
 
 
 def test_solve(pair):
-    _, c, ref, gpu = pair
+    ro, c, ref, gpu = pair
     _, f = ref.seeded_rhs(SEED)
     out = ref.solve(f)
     gpu.set_rhs(f)
     rep = gpu.solve()
     u = gpu.solution()
     assert rep.converged == out["converged"]
+    if ro and c.stencil_mode == "Take":
+        # reference operation order: the whole solve is bitwise identical (the
+        # residual norm is a parallel reduction: equal to 1e-14 relative)
+        assert rep.iterations == out["iterations"]
+        assert np.array_equal(u, out["u"])
+        h = np.array(rep.residual_norms)
+        assert np.allclose(h, out["residual_norms"], rtol=1e-11, atol=0)
+        return
     assert abs(rep.iterations - out["iterations"]) <= 1
     assert relmax(u, out["u"]) < 1e-10
     h = np.array(rep.residual_norms)
