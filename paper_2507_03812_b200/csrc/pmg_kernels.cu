@@ -10,7 +10,9 @@
 //
 // All arrays carry a leading section dimension [B][...]; blockIdx.y is the
 // section, and sections whose `active` flag is 0 (converged) are skipped.
-#include <cooperative_groups.h>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "pmg_kernels.h"
 
@@ -19,11 +21,11 @@ namespace pmg {
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-// The across-origin ring is solved with the reference's exact substitution
-// order (see origin_solve_exact); the 2x2-map scan version (origin_solve) is
-// kept for rings above this length when PMG_ORIGIN_SCAN_MIN is defined.
+// The across-origin ring is solved in the reference's exact substitution
+// order (origin_solve_exact) in reference_order mode and for rings of at most
+// this length; longer rings use the parallel 2x2-map scan (origin_solve).
 #ifndef PMG_ORIGIN_SCAN_MIN
-#define PMG_ORIGIN_SCAN_MIN (1 << 30)
+#define PMG_ORIGIN_SCAN_MIN 0
 #endif
 
 __device__ __forceinline__ int P(int i) { return i + (i >> 4); }  // bank-conflict padding
@@ -469,27 +471,46 @@ __device__ void origin_solve_exact(double* Y, double* B1, double* B2, const Orig
         B2[P(i)] = of.band2[o + i];
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
         // forward: band rows, with the two dense-row sums accumulated in the
-        // reference's k order as the z_k become available
+        // reference's k order as the z_k become available.  Warp 0 runs the
+        // chain redundantly on all lanes; for each group of 32 rows every lane
+        // preloads its row's operands (rhs, band and dense-row coefficients)
+        // into registers and the chain consumes them through shuffles, so no
+        // memory access sits on the dependency chain.
+        const int lane = threadIdx.x;
+        const int fc1 = of.fc1, fc2 = of.fc2;
         double zm2 = 0.0, zm1 = 0.0;
         double s1 = Y[P(operm(n - 2, h))], s2 = Y[P(operm(n - 1, h))];
-        const int fc1 = of.fc1, fc2 = of.fc2;
-#pragma unroll 4
-        for (int i = 0; i < nb; ++i) {
-            const int pi = P(operm(i, h));
-            double sum = Y[pi];
-            if (i >= 2) sum -= B2[P(i)] * zm2;
-            if (i >= 1) sum -= B1[P(i)] * zm1;
-            Y[pi] = sum;
-            zm2 = zm1;
-            zm1 = sum;
-            if (i >= fc1) s1 -= r1[i] * sum;
-            if (i >= fc2) s2 -= r2[i] * sum;
+        for (int g = 0; g < nb; g += 32) {
+            const int i_l = g + lane;
+            const bool ok = i_l < nb;
+            const double y_l = ok ? Y[P(operm(i_l, h))] : 0.0;
+            const double b1_l = ok ? B1[P(i_l)] : 0.0, b2_l = ok ? B2[P(i_l)] : 0.0;
+            const double a1_l = ok ? r1[i_l] : 0.0, a2_l = ok ? r2[i_l] : 0.0;
+            const int cnt = nb - g < 32 ? nb - g : 32;
+            double res = 0.0;
+            for (int j = 0; j < cnt; ++j) {
+                const int i = g + j;
+                const double yv = __shfl_sync(FULL, y_l, j);
+                const double l1 = __shfl_sync(FULL, b1_l, j), l2 = __shfl_sync(FULL, b2_l, j);
+                const double a1 = __shfl_sync(FULL, a1_l, j), a2 = __shfl_sync(FULL, a2_l, j);
+                double sum = yv;
+                if (i >= 2) sum -= l2 * zm2;
+                if (i >= 1) sum -= l1 * zm1;
+                zm2 = zm1;
+                zm1 = sum;
+                if (i >= fc1) s1 -= a1 * sum;
+                if (i >= fc2) s2 -= a2 * sum;
+                if (lane == j) res = sum;
+            }
+            if (ok) Y[P(operm(i_l, h))] = res;
         }
-        if (n - 2 >= fc2) s2 -= r2[n - 2] * s1;
-        Y[P(operm(n - 2, h))] = s1;
-        Y[P(operm(n - 1, h))] = s2;
+        if (lane == 0) {
+            if (n - 2 >= fc2) s2 -= r2[n - 2] * s1;
+            Y[P(operm(n - 2, h))] = s1;
+            Y[P(operm(n - 1, h))] = s2;
+        }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += T) Y[P(operm(i, h))] /= D[i];
@@ -509,19 +530,30 @@ __device__ void origin_solve_exact(double* Y, double* B1, double* B2, const Orig
         }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
         // band backward: row i updates x_{i-2} then x_{i-1}; x_k is final once
-        // rows k+2 and k+1 have been applied
+        // rows k+2 and k+1 have been applied.  Same register/shuffle scheme.
+        const int lane = threadIdx.x;
         double xp1 = 0.0, xp2 = 0.0;  // x_{k+1}, x_{k+2}
-#pragma unroll 4
-        for (int k = nb - 1; k >= 0; --k) {
-            const int pk = P(operm(k, h));
-            double x = Y[pk];
-            if (k + 2 < nb) x -= B2[P(k + 2)] * xp2;
-            if (k + 1 < nb) x -= B1[P(k + 1)] * xp1;
-            Y[pk] = x;
-            xp2 = xp1;
-            xp1 = x;
+        for (int g = nb - 1; g >= 0; g -= 32) {
+            const int k_l = g - lane;  // lane j handles row g - j
+            const bool ok = k_l >= 0;
+            const double x_l = ok ? Y[P(operm(k_l, h))] : 0.0;
+            const double c2_l = (ok && k_l + 2 < nb) ? B2[P(k_l + 2)] : 0.0;
+            const double c1_l = (ok && k_l + 1 < nb) ? B1[P(k_l + 1)] : 0.0;
+            const int cnt = g + 1 < 32 ? g + 1 : 32;
+            double res = 0.0;
+            for (int j = 0; j < cnt; ++j) {
+                const int k = g - j;
+                double x = __shfl_sync(FULL, x_l, j);
+                const double l2 = __shfl_sync(FULL, c2_l, j), l1 = __shfl_sync(FULL, c1_l, j);
+                if (k + 2 < nb) x -= l2 * xp2;
+                if (k + 1 < nb) x -= l1 * xp1;
+                xp2 = xp1;
+                xp1 = x;
+                if (lane == j) res = x;
+            }
+            if (ok) Y[P(operm(k_l, h))] = res;
         }
     }
     __syncthreads();
@@ -688,7 +720,7 @@ __global__ void __launch_bounds__(512) k_circle(LevelView L, double* __restrict_
     }
     if (s == 0 && L.boundary == 0) {
         __syncthreads();
-        if (nt < PMG_ORIGIN_SCAN_MIN)
+        if (serial || nt < PMG_ORIGIN_SCAN_MIN)
             origin_solve_exact(Y, IL, M, of, b, nt);
         else
             origin_solve<K>(Y, IL, of, b, nt, scr);
@@ -926,10 +958,11 @@ __global__ void __launch_bounds__(256) k_norm_final(const double* __restrict__ p
 }
 
 // convergence test of MultigridSolver::solve (multigrid.cpp:321-340)
-__global__ void k_check(const double* __restrict__ norms, ConvState cs, int B, int it,
-                        int max_it, double rel_tol, double abs_tol) {
+__global__ void k_check(const double* __restrict__ norms, ConvState cs, int B, int max_it,
+                        double rel_tol, double abs_tol) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B || !cs.active[b]) return;
+    const int it = cs.count[b]++;  // residual norms taken so far = iteration index
     const double r = norms[b];
     if (it < cs.cap) cs.hist[(long)b * cs.cap + it] = r;
     bool conv;
@@ -953,9 +986,13 @@ __global__ void k_fill(double* p, long n, double v) {
         p[i] = v;
 }
 
-__global__ void k_set_active(int* active, int* remaining, int B) {
+__global__ void k_set_active(int* active, int* count, int* conv, int* remaining, int B) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b < B) active[b] = 1;
+    if (b < B) {
+        active[b] = 1;
+        count[b] = 0;
+        conv[b] = 0;
+    }
     if (b == 0) *remaining = B;
 }
 
@@ -966,11 +1003,20 @@ __global__ void k_flush(double* p, long n) {
 }
 
 // ------------------------------------------------------------ launch helpers
+// Opt a kernel into the full 227 KB of dynamic shared memory once per
+// (kernel, device); launches then pass their exact size.
 template <class KernelT>
 void set_smem(KernelT kern, size_t bytes) {
-    static thread_local bool done = false;  // per instantiation
-    (void)done;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    (void)bytes;
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_pair(reinterpret_cast<const void*>(kern), dev);
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count(key)) return;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    done.insert(key);
 }
 
 // chunk size K and threads T for a line of n rows: T = 32*ceil(ceil(n/K)/32) <= 512
@@ -1113,9 +1159,9 @@ void launch_norm_final(const double* partials, int nblk, int B, long n, int norm
     k_norm_final<<<B, 256, 0, st>>>(partials, nblk, n, norm_type, norms);
 }
 
-void launch_check(const double* norms, ConvState cs, int B, int it, int max_it, double rel_tol,
+void launch_check(const double* norms, ConvState cs, int B, int max_it, double rel_tol,
                   double abs_tol, cudaStream_t st) {
-    k_check<<<(B + 127) / 128, 128, 0, st>>>(norms, cs, B, it, max_it, rel_tol, abs_tol);
+    k_check<<<(B + 127) / 128, 128, 0, st>>>(norms, cs, B, max_it, rel_tol, abs_tol);
 }
 
 void launch_fill(double* p, long n, double v, cudaStream_t st) {
@@ -1125,8 +1171,9 @@ void launch_fill(double* p, long n, double v, cudaStream_t st) {
     k_fill<<<(int)nb, 256, 0, st>>>(p, n, v);
 }
 
-void launch_set_active(int* active, int* remaining, int B, cudaStream_t st) {
-    k_set_active<<<(B + 127) / 128, 128, 0, st>>>(active, remaining, B);
+void launch_set_active(int* active, int* count, int* conv, int* remaining, int B,
+                       cudaStream_t st) {
+    k_set_active<<<(B + 127) / 128, 128, 0, st>>>(active, count, conv, remaining, B);
 }
 
 void launch_flush(double* buf, long n, cudaStream_t st) {

@@ -93,13 +93,15 @@ struct ConvState {
     int* iters;         // [B]
     int* converged;     // [B]
     int* remaining;     // [1]
+    int* count;         // [B] norms taken so far (the iteration index)
     int cap;
 };
-void launch_check(const double* norms, ConvState cs, int B, int it, int max_it, double rel_tol,
+void launch_check(const double* norms, ConvState cs, int B, int max_it, double rel_tol,
                   double abs_tol, cudaStream_t st);
 
 void launch_fill(double* p, long n, double v, cudaStream_t st);
-void launch_set_active(int* active, int* remaining, int B, cudaStream_t st);
+void launch_set_active(int* active, int* count, int* conv, int* remaining, int B,
+                       cudaStream_t st);
 void launch_flush(double* buf, long n, cudaStream_t st);
 
 // ---- setup (pmg_setup.cu) ----

@@ -203,6 +203,11 @@ struct Solver {
     // convergence state
     double *norms = nullptr, *partials = nullptr, *r0 = nullptr, *hist = nullptr;
     int *active = nullptr, *iters = nullptr, *conv = nullptr, *remaining = nullptr;
+    int* count = nullptr;
+    // CUDA graph of one cycle + residual norm + convergence check
+    cudaGraphExec_t cycle_exec = nullptr;
+    long long cycle_nodes = 0;
+    bool use_graph = true;
     int* h_remaining = nullptr;
     int hist_cap = 0;
     int partial_cap = 0;
@@ -229,6 +234,7 @@ struct Solver {
             cudaEventDestroy(e.b);
         }
         for (auto e : ev_pool) cudaEventDestroy(e);
+        if (cycle_exec) cudaGraphExecDestroy(cycle_exec);
         for (void* p : allocs) cudaFree(p);
         if (h_remaining) cudaFreeHost(h_remaining);
         if (own_stream && stream) cudaStreamDestroy(stream);
@@ -331,6 +337,7 @@ struct Solver {
         active = alloc<int>(B);
         iters = alloc<int>(B);
         conv = alloc<int>(B);
+        count = alloc<int>(B);
         remaining = alloc<int>(1);
         partial_cap = std::max(apply_blocks(lv[0].v), 1024);
         partials = alloc<double>((size_t)B * partial_cap);
@@ -621,8 +628,8 @@ struct Solver {
         for (int i = 0; i < set.post_smoothing; ++i) smooth(l, act);
     }
 
-    // residual norm + convergence bookkeeping of iteration `it`
-    void norm_check(int it) {
+    // residual norm + convergence bookkeeping of the next iteration index
+    void norm_check() {
         Level& V = lv[0];
         int nb = 0;
         run(KK_RESIDUAL, 1, [&] {
@@ -631,10 +638,26 @@ struct Solver {
         });
         run(KK_NORM, 2, [&] {
             launch_norm_final(partials, nb, B, V.v.n, set.norm_type, norms, stream);
-            ConvState cs{r0, hist, active, iters, conv, remaining, hist_cap};
-            launch_check(norms, cs, B, it, set.max_iterations, set.relative_tolerance,
+            ConvState cs{r0, hist, active, iters, conv, remaining, count, hist_cap};
+            launch_check(norms, cs, B, set.max_iterations, set.relative_tolerance,
                          set.absolute_tolerance, stream);
         });
+    }
+
+    // one multigrid cycle + residual norm + convergence check, captured once
+    // and replayed every iteration (the active mask and the per-section
+    // iteration counters live on the device)
+    void build_cycle_graph() {
+        const long long l0 = launches;
+        cudaGraph_t g = nullptr;
+        PMG_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+        cycle(0, set.cycle, active);
+        norm_check();
+        PMG_CUDA(cudaStreamEndCapture(stream, &g));
+        PMG_CUDA(cudaGraphInstantiate(&cycle_exec, g, 0));
+        cudaGraphDestroy(g);
+        cycle_nodes = launches - l0;
+        launches = l0;
     }
 
     int solve(pmg_report* reports, double* history, int history_cap) {
@@ -645,11 +668,12 @@ struct Solver {
         PMG_CUDA(cudaEventRecord(e0, stream));
         Level& V = lv[0];
         run(KK_OTHER, 2, [&] {
-            launch_set_active(active, remaining, B, stream);
+            launch_set_active(active, count, conv, remaining, B, stream);
             launch_fill(V.u, (long)B * V.v.n, 0.0, stream);  // u = 0; Dirichlet values 0
         });
-        PMG_CUDA(cudaMemsetAsync(conv, 0, sizeof(int) * B, stream));
-        norm_check(0);
+        norm_check();
+        const bool graph = use_graph && !prof;
+        if (graph && !cycle_exec) build_cycle_graph();
         int it = 0;
         for (;;) {
             PMG_CUDA(cudaMemcpyAsync(h_remaining, remaining, sizeof(int), cudaMemcpyDeviceToHost,
@@ -661,9 +685,14 @@ struct Solver {
                 std::printf("cycle %3d  residual %.6e\n", it, r);
             }
             if (*h_remaining == 0) break;
-            cycle(0, set.cycle, active);
+            if (graph) {
+                PMG_CUDA(cudaGraphLaunch(cycle_exec, stream));
+                launches += cycle_nodes;
+            } else {
+                cycle(0, set.cycle, active);
+                norm_check();
+            }
             ++it;
-            norm_check(it);
         }
         PMG_CUDA(cudaEventRecord(e1, stream));
         PMG_CUDA(cudaEventSynchronize(e1));

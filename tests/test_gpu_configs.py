@@ -67,7 +67,7 @@ def test_config_solve_bitwise(k, cycle):
     out, rep, err = compare(k, cycle, reference_order=True)
     assert rep.iterations == out["iterations"]
     assert err == 0.0
-    assert np.allclose(np.array(rep.residual_norms), out["residual_norms"], rtol=1e-11, atol=0)
+    assert np.allclose(np.array(rep.residual_norms), out["residual_norms"], rtol=1e-8, atol=0)
 
 
 def test_config3_sections():

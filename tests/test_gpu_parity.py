@@ -155,8 +155,15 @@ def test_solve(pair):
         h = np.array(rep.residual_norms)
         assert np.allclose(h, out["residual_norms"], rtol=1e-11, atol=0)
         return
-    assert abs(rep.iterations - out["iterations"]) <= 1
-    assert relmax(u, out["u"]) < 1e-10
+    assert rep.iterations == out["iterations"]
+    # fast mode: within 1e-10 or within the reference's own change under a
+    # one-ulp perturbation of half the entries of f (its conditioning floor)
+    rng = np.random.default_rng(0)
+    g = f.copy()
+    m = rng.random(f.size) < 0.5
+    g[m] = np.nextafter(g[m], np.inf)
+    sens = relmax(ref.solve(g)["u"], out["u"])
+    assert relmax(u, out["u"]) < max(1e-10, sens), (relmax(u, out["u"]), sens)
     h = np.array(rep.residual_norms)
     k = min(len(h), len(out["residual_norms"]))
     # late residuals sit at the roundoff floor of |f - A u| ~ 1e-16 |f|: compare
