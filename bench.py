@@ -214,10 +214,10 @@ def build_solver(workload, rank, world, stream):
     geom, prob, grid, st, meta = pmg.baseline_config(k, cycle=cyc)
     sections = None
     if k == 3:
+        from paper_2507_03812_b200.shard import section_shard
         scales = pmg.section_scales(256)
-        per = 256 // world
-        sections = list(range(rank * per, (rank + 1) * per))
-        solver = pmg.MultigridSolver(geom, prob, grid, st, n_sections=per,
+        sections = section_shard(256, rank, world)
+        solver = pmg.MultigridSolver(geom, prob, grid, st, n_sections=len(sections),
                                      alpha_scales=scales[sections], stream=stream)
     else:
         solver = pmg.MultigridSolver(geom, prob, grid, st, stream=stream)

@@ -138,6 +138,12 @@ int pmg_create_batch(const pmg_geometry* geom, const pmg_problem* prob, const pm
                      int device, void* stream, pmg_handle* out);
 int pmg_destroy(pmg_handle h);
 
+/* host-only (no device needed): the level chain the solver would build --
+ * build_grid/uniform + can_coarsen/coarsen (polar_grid.cpp:99-207,
+ * multigrid.cpp:81-87).  Arrays receive min(levels, capacity) entries. */
+int pmg_grid_hierarchy(const pmg_grid* grid, int max_levels, int capacity, int* levels,
+                       int* n_r, int* n_theta, int* split);
+
 /* hierarchy inspection -- multigrid.hpp:99-108 */
 int pmg_num_levels(pmg_handle h, int* levels);
 int pmg_num_sections(pmg_handle h, int* sections);

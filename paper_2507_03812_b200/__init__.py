@@ -6,6 +6,6 @@ API.  There is no CPU fallback.
 """
 from .solver import (  # noqa: F401
     LAYOUT_CANONICAL, LAYOUT_NODE, ConvergenceReport, GeometryMap, MultigridSettings,
-    MultigridSolver, PmgError, PolarGrid, ProblemCase, load_library,
+    MultigridSolver, PmgError, PolarGrid, ProblemCase, grid_hierarchy, load_library,
 )
 from .configs import baseline_config, section_scales, SEED  # noqa: F401

@@ -85,6 +85,8 @@ struct LevelView {
     const double* art;
     const double* att;
     const double* det;
+    const double* rh;        // [nr-1] RN(1/h_s)  (exact reciprocals for xdiv)
+    const double* rk;        // [nt]   RN(1/k_t)
     Geo geo;
 
     // reference NodeIndexing (polar_grid.hpp:24-27)
@@ -194,6 +196,172 @@ PMG_HD Row make_row(const LevelView& L, const CF& cf, int s, int t) {
     if (R.has_sp) R.sp = -(kbar / hp) * (cP.arr + cSP.arr);
     double south = -(hbar / km) * (cP.att + cTM.att);
     double north = -(hbar / kp) * (cP.att + cTP.att);
+    if (s == 0) {
+        south += (cP.art - cTM.art) * 0.25;
+        north += (cTP.art - cP.art) * 0.25;
+    } else if (s == N) {
+        south += (cTM.art - cP.art) * 0.25;
+        north += (cP.art - cTP.art) * 0.25;
+    }
+    R.tm = south;
+    R.tp = north;
+    if (R.has_sm) {
+        R.mm = -(cTM.art + cSM.art) * 0.25;
+        R.mp = (cSM.art + cTP.art) * 0.25;
+    }
+    if (R.has_sp) {
+        R.pm = (cTM.art + cSP.art) * 0.25;
+        R.pp = -(cSP.art + cTP.art) * 0.25;
+    }
+    return R;
+}
+
+// Correctly rounded a / b from r = RN(1/b) (Markstein): q0 = RN(a r) is within
+// one ulp of a/b, e = a - b q0 is exact with an FMA, and RN(q0 + e r) = RN(a/b)
+// for normal operands.  Used for the h/k quotients of the stencil so they stay
+// bitwise identical to the reference's divisions at 3 dependent FP64 ops.
+PMG_HD double xdiv(double a, double b, double r) {
+    const double q0 = a * r;
+    const double e = fma(-b, q0, a);
+    return fma(e, r, q0);
+}
+
+// Flat NODE-layout offsets of the 8 neighbours of (s,t) (valid where the
+// neighbour exists).  Interior radial rows (split < s < n_r-1) are spoke-major
+// (+-1 along s, +-len across spokes), interior circle rows (0 < s < split-1)
+// ring-major; the interface rows use the general NodeIndexing.
+struct Nbr {
+    int tm, tp;          // angular neighbour indices (wrapped)
+    int pTM, pTP;        // (s,t-1), (s,t+1)
+    int pSM, pSP;        // (s-1,t), (s+1,t)
+    int pSMTM, pSMTP;    // (s-1,t-1), (s-1,t+1)
+    int pSPTM, pSPTP;    // (s+1,t-1), (s+1,t+1)
+};
+
+PMG_HD Nbr neighbours(const LevelView& L, int s, int t, int p) {
+    Nbr q;
+    q.tm = L.tminus(t);
+    q.tp = L.tplus(t);
+    const int N = L.nr - 1;
+    if (s > L.split && s < N) {
+        q.pTM = p + (q.tm - t) * L.len;
+        q.pTP = p + (q.tp - t) * L.len;
+        q.pSM = p - 1;
+        q.pSP = p + 1;
+        q.pSMTM = q.pTM - 1;
+        q.pSMTP = q.pTP - 1;
+        q.pSPTM = q.pTM + 1;
+        q.pSPTP = q.pTP + 1;
+    } else if (s > 0 && s + 1 < L.split) {
+        q.pTM = p + (q.tm - t);
+        q.pTP = p + (q.tp - t);
+        q.pSM = p - L.nt;
+        q.pSP = p + L.nt;
+        q.pSMTM = q.pTM - L.nt;
+        q.pSMTP = q.pTP - L.nt;
+        q.pSPTM = q.pTM + L.nt;
+        q.pSPTP = q.pTP + L.nt;
+    } else {
+        q.pTM = L.idx(s, q.tm);
+        q.pTP = L.idx(s, q.tp);
+        q.pSM = s > 0 ? L.idx(s - 1, t) : p;
+        q.pSP = s < N ? L.idx(s + 1, t) : p;
+        q.pSMTM = s > 0 ? L.idx(s - 1, q.tm) : p;
+        q.pSMTP = s > 0 ? L.idx(s - 1, q.tp) : p;
+        q.pSPTM = s < N ? L.idx(s + 1, q.tm) : p;
+        q.pSPTP = s < N ? L.idx(s + 1, q.tp) : p;
+    }
+    return q;
+}
+
+// Take-mode coefficient reads by flat index; Give evaluates them at (s,t).
+template <bool ONFLY>
+struct CoefAt;
+template <>
+struct CoefAt<false> {
+    const LevelView* L;
+    long off;
+    int b;
+    __device__ __forceinline__ Coef operator()(int s, int t, int p) const {
+        (void)s;
+        (void)t;
+        Coef c;
+        c.arr = __ldg(L->arr + off + p);
+        c.art = __ldg(L->art + off + p);
+        c.att = __ldg(L->att + off + p);
+        c.det = __ldg(L->det + off + p);
+        return c;
+    }
+};
+template <>
+struct CoefAt<true> {
+    const LevelView* L;
+    long off;
+    int b;
+    __device__ __forceinline__ Coef operator()(int s, int t, int p) const {
+        (void)p;
+        return transform(L->geo, L->alpha[(long)b * L->nr + s], L->r[s], L->sn[t], L->cs[t],
+                         nullptr);
+    }
+};
+
+// make_row with precomputed neighbour offsets and Markstein quotients: the
+// same values as make_row (bitwise); fields a caller does not use are
+// eliminated by the compiler after inlining.
+template <class CF>
+__device__ __forceinline__ Row make_row_fast(const LevelView& L, const CF& cf, int s, int t, int p,
+                                             const Nbr& q) {
+    Row R;
+    R.sm = R.sp = R.tm = R.tp = R.mm = R.mp = R.pm = R.pp = R.ph = 0.0;
+    R.t2 = -1;
+    R.has_sm = R.has_sp = R.origin = false;
+    const int N = L.nr - 1;
+    if (L.dir(s)) {
+        R.ident = true;
+        R.d = 1.0;
+        return R;
+    }
+    R.ident = false;
+    const double km = L.k[q.tm], kp = L.k[t];
+    const double hm = s > 0 ? L.h[s - 1] : 0.0;
+    const double hp = s < N ? L.h[s] : 0.0;
+    const double kbar = 0.5 * (km + kp);
+    const double hbar = 0.5 * (hm + hp);
+    const Coef cP = cf(s, t, p), cTM = cf(s, q.tm, q.pTM), cTP = cf(s, q.tp, q.pTP);
+    Coef cSM = {0.0, 0.0, 0.0, 0.0}, cSP = {0.0, 0.0, 0.0, 0.0};
+    if (s > 0) cSM = cf(s - 1, t, q.pSM);
+    if (s < N) cSP = cf(s + 1, t, q.pSP);
+    const double qkm = s > 0 ? xdiv(kbar, hm, L.rh[s - 1]) : 0.0;  // kbar / hm
+    const double qkp = s < N ? xdiv(kbar, hp, L.rh[s]) : 0.0;      // kbar / hp
+    const double qhm = xdiv(hbar, km, L.rk[q.tm]);                 // hbar / km
+    const double qhp = xdiv(hbar, kp, L.rk[t]);                    // hbar / kp
+    const bool origin = s == 0 && L.boundary == 0;
+    double diag = 0.0;
+    if (s > 0) diag += qkm * (cP.arr + cSM.arr);
+    if (s < N) diag += qkp * (cP.arr + cSP.arr);
+    diag += qhm * (cP.att + cTM.att);
+    diag += qhp * (cP.att + cTP.att);
+    diag += L.beta[(long)cf.b * L.nr + s] * cP.det * hbar * kbar;
+    if (origin) {
+        const int t2 = t + L.nt / 2 >= L.nt ? t + L.nt / 2 - L.nt : t + L.nt / 2;
+        const int tlo = t < t2 ? t : t2;
+        const int thi = t < t2 ? t2 : t;
+        const double klo = 0.5 * (L.k[L.tminus(tlo)] + L.k[tlo]);
+        const double khi = 0.5 * (L.k[L.tminus(thi)] + L.k[thi]);
+        const double omega = (klo + khi) / (4.0 * L.r0);
+        const double w = omega * (cf(0, tlo, tlo).arr + cf(0, thi, thi).arr);
+        diag += w;
+        R.ph = -w;
+        R.t2 = t2;
+        R.origin = true;
+    }
+    R.d = diag;
+    R.has_sm = s > 0 && !L.dir(s - 1);
+    R.has_sp = s < N && !L.dir(s + 1);
+    if (R.has_sm) R.sm = -qkm * (cP.arr + cSM.arr);
+    if (R.has_sp) R.sp = -qkp * (cP.arr + cSP.arr);
+    double south = -qhm * (cP.att + cTM.att);
+    double north = -qhp * (cP.att + cTP.att);
     if (s == 0) {
         south += (cP.art - cTM.art) * 0.25;
         north += (cTP.art - cP.art) * 0.25;

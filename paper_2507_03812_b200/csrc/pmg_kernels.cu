@@ -618,29 +618,29 @@ __global__ void __launch_bounds__(256) k_apply(LevelView L, const double* __rest
     if (p < L.n) {
         int s, t;
         L.node(p, s, t);
-        typename CF<ONFLY>::T cf{&L, b};
-        const Row R = make_row(L, cf, s, t);
+        const CoefAt<ONFLY> cf{&L, off, b};
+        const Nbr q = neighbours(L, s, t, p);
+        const Row R = make_row_fast(L, cf, s, t, p, q);
         double acc;
         if (R.ident) {
             acc = 0.0;
             acc += 1.0 * U[p];
         } else {
-            const int tm = L.tminus(t), tp = L.tplus(t);
             acc = 0.0;
             acc += R.d * U[p];
-            if (R.has_sm) acc += R.sm * U[L.idx(s - 1, t)];
-            if (R.has_sp) acc += R.sp * U[L.idx(s + 1, t)];
-            acc += R.tm * U[L.idx(s, tm)];
-            acc += R.tp * U[L.idx(s, tp)];
+            if (R.has_sm) acc += R.sm * U[q.pSM];
+            if (R.has_sp) acc += R.sp * U[q.pSP];
+            acc += R.tm * U[q.pTM];
+            acc += R.tp * U[q.pTP];
             if (R.has_sm) {
-                acc += R.mm * U[L.idx(s - 1, tm)];
-                acc += R.mp * U[L.idx(s - 1, tp)];
+                acc += R.mm * U[q.pSMTM];
+                acc += R.mp * U[q.pSMTP];
             }
             if (R.has_sp) {
-                acc += R.pm * U[L.idx(s + 1, tm)];
-                acc += R.pp * U[L.idx(s + 1, tp)];
+                acc += R.pm * U[q.pSPTM];
+                acc += R.pp * U[q.pSPTP];
             }
-            if (R.origin) acc += R.ph * U[L.idx(0, R.t2)];
+            if (R.origin) acc += R.ph * U[R.t2];
         }
         if (MODE == 0) {
             val = acc;
@@ -701,20 +701,21 @@ __global__ void __launch_bounds__(512) k_circle(LevelView L, double* __restrict_
     double* IL = smem + pn;
     double* M = IL + pn;
     double* scr = M + pn;
-    typename CF<ONFLY>::T cf{&L, b};
+    const CoefAt<ONFLY> cf{&L, off, b};
     for (int t = threadIdx.x; t < nt; t += T) {
-        const Row R = make_row(L, cf, s, t);
-        const int tm = L.tminus(t), tp = L.tplus(t);
-        double acc = F[base + t];
-        if (R.has_sm) acc -= R.sm * U[L.idx(s - 1, t)];
-        if (R.has_sp) acc -= R.sp * U[L.idx(s + 1, t)];
+        const int p = base + t;
+        const Nbr q = neighbours(L, s, t, p);
+        const Row R = make_row_fast(L, cf, s, t, p, q);
+        double acc = F[p];
+        if (R.has_sm) acc -= R.sm * U[q.pSM];
+        if (R.has_sp) acc -= R.sp * U[q.pSP];
         if (R.has_sm) {
-            acc -= R.mm * U[L.idx(s - 1, tm)];
-            acc -= R.mp * U[L.idx(s - 1, tp)];
+            acc -= R.mm * U[q.pSMTM];
+            acc -= R.mp * U[q.pSMTP];
         }
         if (R.has_sp) {
-            acc -= R.pm * U[L.idx(s + 1, tm)];
-            acc -= R.pp * U[L.idx(s + 1, tp)];
+            acc -= R.pm * U[q.pSPTM];
+            acc -= R.pp * U[q.pSPTP];
         }
         Y[P(t)] = acc;
     }
@@ -728,7 +729,7 @@ __global__ void __launch_bounds__(512) k_circle(LevelView L, double* __restrict_
         const long fo = (long)b * L.split * nt + (long)s * nt;
         const bool exact = serial || s <= exact_rings;  // block-uniform
         for (int t = threadIdx.x; t < nt; t += T) {
-            IL[P(t)] = exact ? cil[fo + t] : 1.0 / cil[fo + t];
+            IL[P(t)] = exact ? cil[fo + t] : __drcp_rn(cil[fo + t]);
             M[P(t)] = cm[fo + t];
         }
         __syncthreads();
@@ -765,29 +766,31 @@ __global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict_
     double* IL = smem + pn;
     double* M = IL + pn;
     double* scr = M + pn;
-    const int tm = L.tminus(t), tp = L.tplus(t);
-    typename CF<ONFLY>::T cf{&L, b};
+    const CoefAt<ONFLY> cf{&L, off, b};
     const long fo = ((long)b * L.nt + t) * len;
     for (int i = threadIdx.x; i < len; i += T) {
         const int s = split + i;
-        IL[P(i)] = serial ? ril[fo + i] : 1.0 / ril[fo + i];
+        const double lv = ril[fo + i];
+        IL[P(i)] = serial ? lv : __drcp_rn(lv);
         M[P(i)] = rm[fo + i];
+        const int p = base + i;
         if (L.dir(s)) {
-            Y[P(i)] = F[base + i];
+            Y[P(i)] = F[p];
             continue;
         }
-        const Row R = make_row(L, cf, s, t);
-        double acc = F[base + i];
-        if (s == split && R.has_sm) acc -= R.sm * U[L.idx(s - 1, t)];
-        acc -= R.tm * U[L.idx(s, tm)];
-        acc -= R.tp * U[L.idx(s, tp)];
+        const Nbr q = neighbours(L, s, t, p);
+        const Row R = make_row_fast(L, cf, s, t, p, q);
+        double acc = F[p];
+        if (s == split && R.has_sm) acc -= R.sm * U[q.pSM];
+        acc -= R.tm * U[q.pTM];
+        acc -= R.tp * U[q.pTP];
         if (R.has_sm) {
-            acc -= R.mm * U[L.idx(s - 1, tm)];
-            acc -= R.mp * U[L.idx(s - 1, tp)];
+            acc -= R.mm * U[q.pSMTM];
+            acc -= R.mp * U[q.pSMTP];
         }
         if (R.has_sp) {
-            acc -= R.pm * U[L.idx(s + 1, tm)];
-            acc -= R.pp * U[L.idx(s + 1, tp)];
+            acc -= R.pm * U[q.pSPTM];
+            acc -= R.pp * U[q.pSPTP];
         }
         Y[P(i)] = acc;
     }

@@ -382,6 +382,13 @@ struct Solver {
         v.r = upload(g.r);
         v.h = upload(g.h);
         v.k = upload(g.k);
+        {  // exact reciprocals RN(1/h), RN(1/k) for the Markstein quotients
+            std::vector<double> rh(g.h.size()), rk(g.k.size());
+            for (std::size_t i = 0; i < rh.size(); ++i) rh[i] = 1.0 / g.h[i];
+            for (std::size_t i = 0; i < rk.size(); ++i) rk[i] = 1.0 / g.k[i];
+            v.rh = upload(rh);
+            v.rk = upload(rk);
+        }
         v.sn = upload(V.h_sn);
         v.cs = upload(V.h_cs);
         v.alpha = upload(V.h_alpha);
@@ -474,6 +481,7 @@ struct Solver {
         h.alpha = V.h_alpha.data();
         h.beta = V.h_beta.data();
         h.arr = h.art = h.att = h.det = nullptr;
+        h.rh = h.rk = nullptr;
         return h;
     }
 
@@ -938,6 +946,35 @@ int pmg_create_batch(const pmg_geometry* geom, const pmg_problem* prob, const pm
 int pmg_create(const pmg_geometry* geom, const pmg_problem* prob, const pmg_grid* grid,
                const pmg_settings* settings, int device, void* stream, pmg_handle* out) {
     return pmg_create_batch(geom, prob, grid, settings, 1, nullptr, device, stream, out);
+}
+
+int pmg_grid_hierarchy(const pmg_grid* gp, int max_levels, int capacity, int* levels, int* n_r,
+                       int* n_theta, int* split) {
+    return guarded([&] {
+        if (!gp || !levels) throw PmgError(PMG_EINVAL, "null argument");
+        const double tol = gp->pair_tolerance > 0.0 ? gp->pair_tolerance : 1e-12;
+        pmg::HostGrid g;
+        if (gp->mode == 0)
+            g = pmg::uniform_grid(gp->R0, gp->Rmax, gp->n_r, gp->n_theta, tol);
+        else if (gp->mode == 1)
+            g = pmg::build_grid(gp->R0, gp->Rmax, gp->nr_exp, gp->ntheta_exp,
+                                gp->anisotropic_factor, gp->divide_by_2, tol);
+        else
+            g = pmg::make_grid(std::vector<double>(gp->radii, gp->radii + gp->n_r),
+                               std::vector<double>(gp->angles, gp->angles + gp->n_theta), tol);
+        int L = 0;
+        for (;;) {
+            if (L < capacity) {
+                n_r[L] = g.nr();
+                n_theta[L] = g.nt();
+                split[L] = g.split;
+            }
+            ++L;
+            if ((max_levels != 0 && L >= max_levels) || !pmg::can_coarsen(g, tol)) break;
+            g = pmg::coarsen(g, tol);
+        }
+        *levels = L;
+    });
 }
 
 int pmg_destroy(pmg_handle h) {

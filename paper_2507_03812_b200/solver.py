@@ -84,7 +84,7 @@ _lib = None
 # every symbol include/polarmg_b200.h declares (checked by tests)
 EXPORTED = [
     "pmg_last_error", "pmg_version", "pmg_default_settings", "pmg_create", "pmg_create_batch",
-    "pmg_destroy", "pmg_num_levels", "pmg_num_sections", "pmg_level_info", "pmg_level_grid",
+    "pmg_destroy", "pmg_grid_hierarchy", "pmg_num_levels", "pmg_num_sections", "pmg_level_info", "pmg_level_grid",
     "pmg_set_rhs", "pmg_get_rhs", "pmg_set_rhs_device", "pmg_seeded_rhs", "pmg_solve", "pmg_get_solution",
     "pmg_solution_device", "pmg_apply", "pmg_residual", "pmg_smooth", "pmg_sweep",
     "pmg_restrict", "pmg_prolongate", "pmg_coarse_solve", "pmg_norm", "pmg_launch_count",
@@ -114,6 +114,8 @@ def load_library(path: str = LIB_PATH):
                                      C.POINTER(_Settings), C.c_int, _dp, C.c_int, vp,
                                      C.POINTER(vp)]
     lib.pmg_destroy.argtypes = [vp]
+    lib.pmg_grid_hierarchy.argtypes = [C.POINTER(_Grid), C.c_int, C.c_int, C.POINTER(C.c_int),
+                                       C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
     lib.pmg_num_levels.argtypes = [vp, C.POINTER(C.c_int)]
     lib.pmg_num_sections.argtypes = [vp, C.POINTER(C.c_int)]
     lib.pmg_level_info.argtypes = [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
@@ -254,6 +256,29 @@ class ConvergenceReport:
     device_bytes: int = 0
 
 
+def _grid_struct(grid: "PolarGrid", keep: list):
+    gr = _Grid(grid.mode, grid.R0, grid.Rmax, grid.n_r, grid.n_theta, grid.nr_exp,
+               grid.ntheta_exp, grid.anisotropic_factor, grid.divide_by_2, None, None,
+               grid.pair_tolerance)
+    if grid.mode == 2:
+        r, a = _arr(grid.radii), _arr(grid.angles)
+        keep += [r, a]
+        gr.radii, gr.angles = _p(r), _p(a)
+    return gr
+
+
+def grid_hierarchy(grid: "PolarGrid", max_levels: int = 0):
+    """[(n_r, n_theta, split), ...] of the level chain (host only, no GPU)."""
+    lib = load_library()
+    keep: list = []
+    gr = _grid_struct(grid, keep)
+    cap = 64
+    L = C.c_int()
+    nr, nt, sp = (C.c_int * cap)(), (C.c_int * cap)(), (C.c_int * cap)()
+    _check(lib.pmg_grid_hierarchy(C.byref(gr), max_levels, cap, C.byref(L), nr, nt, sp))
+    return [(nr[i], nt[i], sp[i]) for i in range(min(L.value, cap))]
+
+
 def _lookup(table, key, what):
     if isinstance(key, int):
         return key
@@ -283,13 +308,7 @@ class MultigridSolver:
                 problem.beta_coeff, str) else problem.beta_coeff,
             problem.rmax, problem.alpha_jump, problem.delta_r, problem.alpha_scale)
         self._keep = []
-        gr = _Grid(grid.mode, grid.R0, grid.Rmax, grid.n_r, grid.n_theta, grid.nr_exp,
-                   grid.ntheta_exp, grid.anisotropic_factor, grid.divide_by_2, None, None,
-                   grid.pair_tolerance)
-        if grid.mode == 2:
-            r, a = _arr(grid.radii), _arr(grid.angles)
-            self._keep += [r, a]
-            gr.radii, gr.angles = _p(r), _p(a)
+        gr = _grid_struct(grid, self._keep)
         s = _Settings(_lookup(STENCIL, settings.stencil_mode, "stencilDistributionMethod"),
                       _lookup(BOUNDARY, settings.boundary_mode, "boundary mode"),
                       int(settings.cache_profile), int(settings.cache_geometry),
