@@ -286,10 +286,10 @@ struct CoefAt<false> {
         (void)s;
         (void)t;
         Coef c;
-        c.arr = __ldg(L->arr + off + p);
-        c.art = __ldg(L->art + off + p);
-        c.att = __ldg(L->att + off + p);
-        c.det = __ldg(L->det + off + p);
+        c.arr = L->arr[off + p];
+        c.art = L->art[off + p];
+        c.att = L->att[off + p];
+        c.det = L->det[off + p];
         return c;
     }
 };
@@ -308,9 +308,14 @@ struct CoefAt<true> {
 // make_row with precomputed neighbour offsets and Markstein quotients: the
 // same values as make_row (bitwise); fields a caller does not use are
 // eliminated by the compiler after inlining.
-template <class CF>
-__device__ __forceinline__ Row make_row_fast(const LevelView& L, const CF& cf, int s, int t, int p,
-                                             const Nbr& q) {
+// Row of (s,t) from the coefficients of the node and its four neighbours
+// (no loads; the origin-ring phantom weight needs arr of the antipodal node,
+// passed in arrAnti).  Same expressions and order as make_row
+// (stencil.cpp:44-137); h/k quotients by Markstein division.
+__host__ __device__ __forceinline__ Row row_from(const LevelView& L, int b, int s, int t, int tm,
+                                                 const Coef& cP, const Coef& cTM,
+                                                 const Coef& cTP, const Coef& cSM,
+                                                 const Coef& cSP, double arrAnti) {
     Row R;
     R.sm = R.sp = R.tm = R.tp = R.mm = R.mp = R.pm = R.pp = R.ph = 0.0;
     R.t2 = -1;
@@ -322,34 +327,30 @@ __device__ __forceinline__ Row make_row_fast(const LevelView& L, const CF& cf, i
         return R;
     }
     R.ident = false;
-    const double km = L.k[q.tm], kp = L.k[t];
+    const double km = L.k[tm], kp = L.k[t];
     const double hm = s > 0 ? L.h[s - 1] : 0.0;
     const double hp = s < N ? L.h[s] : 0.0;
     const double kbar = 0.5 * (km + kp);
     const double hbar = 0.5 * (hm + hp);
-    const Coef cP = cf(s, t, p), cTM = cf(s, q.tm, q.pTM), cTP = cf(s, q.tp, q.pTP);
-    Coef cSM = {0.0, 0.0, 0.0, 0.0}, cSP = {0.0, 0.0, 0.0, 0.0};
-    if (s > 0) cSM = cf(s - 1, t, q.pSM);
-    if (s < N) cSP = cf(s + 1, t, q.pSP);
     const double qkm = s > 0 ? xdiv(kbar, hm, L.rh[s - 1]) : 0.0;  // kbar / hm
     const double qkp = s < N ? xdiv(kbar, hp, L.rh[s]) : 0.0;      // kbar / hp
-    const double qhm = xdiv(hbar, km, L.rk[q.tm]);                 // hbar / km
+    const double qhm = xdiv(hbar, km, L.rk[tm]);                   // hbar / km
     const double qhp = xdiv(hbar, kp, L.rk[t]);                    // hbar / kp
-    const bool origin = s == 0 && L.boundary == 0;
     double diag = 0.0;
     if (s > 0) diag += qkm * (cP.arr + cSM.arr);
     if (s < N) diag += qkp * (cP.arr + cSP.arr);
     diag += qhm * (cP.att + cTM.att);
     diag += qhp * (cP.att + cTP.att);
-    diag += L.beta[(long)cf.b * L.nr + s] * cP.det * hbar * kbar;
-    if (origin) {
+    diag += L.beta[(long)b * L.nr + s] * cP.det * hbar * kbar;
+    if (s == 0 && L.boundary == 0) {
         const int t2 = t + L.nt / 2 >= L.nt ? t + L.nt / 2 - L.nt : t + L.nt / 2;
         const int tlo = t < t2 ? t : t2;
         const int thi = t < t2 ? t2 : t;
         const double klo = 0.5 * (L.k[L.tminus(tlo)] + L.k[tlo]);
         const double khi = 0.5 * (L.k[L.tminus(thi)] + L.k[thi]);
         const double omega = (klo + khi) / (4.0 * L.r0);
-        const double w = omega * (cf(0, tlo, tlo).arr + cf(0, thi, thi).arr);
+        const double alo = t < t2 ? cP.arr : arrAnti, ahi = t < t2 ? arrAnti : cP.arr;
+        const double w = omega * (alo + ahi);
         diag += w;
         R.ph = -w;
         R.t2 = t2;
@@ -380,6 +381,32 @@ __device__ __forceinline__ Row make_row_fast(const LevelView& L, const CF& cf, i
         R.pp = -(cSP.art + cTP.art) * 0.25;
     }
     return R;
+}
+
+// make_row with precomputed neighbour offsets: loads then row_from.
+template <class CF>
+__device__ __forceinline__ Row make_row_fast(const LevelView& L, const CF& cf, int s, int t, int p,
+                                             const Nbr& q) {
+    const int N = L.nr - 1;
+    if (L.dir(s)) {
+        Row R;
+        R.sm = R.sp = R.tm = R.tp = R.mm = R.mp = R.pm = R.pp = R.ph = 0.0;
+        R.t2 = -1;
+        R.has_sm = R.has_sp = R.origin = false;
+        R.ident = true;
+        R.d = 1.0;
+        return R;
+    }
+    const Coef z = {0.0, 0.0, 0.0, 0.0};
+    const Coef cP = cf(s, t, p), cTM = cf(s, q.tm, q.pTM), cTP = cf(s, q.tp, q.pTP);
+    const Coef cSM = s > 0 ? cf(s - 1, t, q.pSM) : z;
+    const Coef cSP = s < N ? cf(s + 1, t, q.pSP) : z;
+    double anti = 0.0;
+    if (s == 0 && L.boundary == 0) {
+        const int t2 = t + L.nt / 2 >= L.nt ? t + L.nt / 2 - L.nt : t + L.nt / 2;
+        anti = cf(0, t2, t2).arr;  // ring 0 is ring-major: flat index t2
+    }
+    return row_from(L, cf.b, s, t, q.tm, cP, cTM, cTP, cSM, cSP, anti);
 }
 
 }  // namespace pmg

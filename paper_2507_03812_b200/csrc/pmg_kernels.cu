@@ -10,6 +10,8 @@
 //
 // All arrays carry a leading section dimension [B][...]; blockIdx.y is the
 // section, and sections whose `active` flag is 0 (converged) are skipped.
+#include <cuda_pipeline.h>
+
 #include <mutex>
 #include <set>
 #include <utility>
@@ -603,55 +605,98 @@ __device__ void origin_solve_serial(double* Y, double* X, const OriginFactor& of
 // ------------------------------------------------------------ apply / residual
 // y = A u or r = f - A u with the Take/Give row of stencil.cpp:44-137 and the
 // accumulation order of apply_take (stencil.cpp:166-171).
+// All operands of one row gathered into registers before any arithmetic, so
+// the ~22 independent loads of a node are in flight together (the kernel is
+// memory-latency bound otherwise).  Absent neighbours read the node itself.
+struct Gather {
+    double u, uSM, uSP, uTM, uTP, uSMTM, uSMTP, uSPTM, uSPTP, f;
+    Coef P, TM, TP, SM, SP;
+};
+
+template <bool ONFLY, int MODE>
+__device__ __forceinline__ double apply_node(const LevelView& L, const double* __restrict__ U,
+                                             const double* __restrict__ F, long off, int b,
+                                             int p) {
+    int s, t;
+    L.node(p, s, t);
+    const Nbr q = neighbours(L, s, t, p);
+    const CoefAt<ONFLY> cf{&L, off, b};
+    if (L.dir(s)) {  // identity row
+        double acc = 0.0;
+        acc += 1.0 * U[p];
+        return MODE == 0 ? acc : F[p] - acc;
+    }
+    const int N = L.nr - 1;
+    const bool hs = s > 0, hp = s < N;
+    Gather g;
+    g.u = U[p];
+    g.uTM = U[q.pTM];
+    g.uTP = U[q.pTP];
+    g.uSM = U[hs ? q.pSM : p];
+    g.uSMTM = U[hs ? q.pSMTM : p];
+    g.uSMTP = U[hs ? q.pSMTP : p];
+    g.uSP = U[hp ? q.pSP : p];
+    g.uSPTM = U[hp ? q.pSPTM : p];
+    g.uSPTP = U[hp ? q.pSPTP : p];
+    g.f = MODE == 0 ? 0.0 : F[p];
+    g.P = cf(s, t, p);
+    g.TM = cf(s, q.tm, q.pTM);
+    g.TP = cf(s, q.tp, q.pTP);
+    g.SM = hs ? cf(s - 1, t, q.pSM) : Coef{0.0, 0.0, 0.0, 0.0};
+    g.SP = hp ? cf(s + 1, t, q.pSP) : Coef{0.0, 0.0, 0.0, 0.0};
+    double anti = 0.0;
+    if (s == 0 && L.boundary == 0) {
+        const int t2 = t + L.nt / 2 >= L.nt ? t + L.nt / 2 - L.nt : t + L.nt / 2;
+        anti = cf(0, t2, t2).arr;
+    }
+    const Row R = row_from(L, b, s, t, q.tm, g.P, g.TM, g.TP, g.SM, g.SP, anti);
+    double acc = 0.0;
+    acc += R.d * g.u;
+    if (R.has_sm) acc += R.sm * g.uSM;
+    if (R.has_sp) acc += R.sp * g.uSP;
+    acc += R.tm * g.uTM;
+    acc += R.tp * g.uTP;
+    if (R.has_sm) {
+        acc += R.mm * g.uSMTM;
+        acc += R.mp * g.uSMTP;
+    }
+    if (R.has_sp) {
+        acc += R.pm * g.uSPTM;
+        acc += R.pp * g.uSPTP;
+    }
+    if (R.origin) acc += R.ph * U[R.t2];
+    return MODE == 0 ? acc : g.f - acc;
+}
+
+// y = A u (MODE 0) or r = f - A u (MODE 1), NPT nodes per thread; optional
+// per-block partial sums of r^2 (or max |r|) for the residual norm.
 template <bool ONFLY, int MODE, bool NORM>
 __global__ void __launch_bounds__(256) k_apply(LevelView L, const double* __restrict__ u,
                                                const double* __restrict__ f,
                                                double* __restrict__ out,
                                                double* __restrict__ partials, int norm_type,
                                                const int* __restrict__ active) {
+    constexpr int NPT = 2;
     const int b = blockIdx.y;
     if (active && !active[b]) return;
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
     const long off = (long)b * L.n;
     const double* U = u + off;
-    double val = 0.0;
-    if (p < L.n) {
-        int s, t;
-        L.node(p, s, t);
-        const CoefAt<ONFLY> cf{&L, off, b};
-        const Nbr q = neighbours(L, s, t, p);
-        const Row R = make_row_fast(L, cf, s, t, p, q);
-        double acc;
-        if (R.ident) {
-            acc = 0.0;
-            acc += 1.0 * U[p];
-        } else {
-            acc = 0.0;
-            acc += R.d * U[p];
-            if (R.has_sm) acc += R.sm * U[q.pSM];
-            if (R.has_sp) acc += R.sp * U[q.pSP];
-            acc += R.tm * U[q.pTM];
-            acc += R.tp * U[q.pTP];
-            if (R.has_sm) {
-                acc += R.mm * U[q.pSMTM];
-                acc += R.mp * U[q.pSMTP];
-            }
-            if (R.has_sp) {
-                acc += R.pm * U[q.pSPTM];
-                acc += R.pp * U[q.pSPTP];
-            }
-            if (R.origin) acc += R.ph * U[R.t2];
-        }
-        if (MODE == 0) {
-            val = acc;
-        } else {
-            val = f[off + p] - acc;
-        }
-        out[off + p] = val;
+    const double* F = MODE == 0 ? nullptr : f + off;
+    double v = 0.0;
+    double val[NPT];
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+        const int p = (blockIdx.x * NPT + k) * blockDim.x + threadIdx.x;
+        val[k] = p < L.n ? apply_node<ONFLY, MODE>(L, U, F, off, b, p) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+        const int p = (blockIdx.x * NPT + k) * blockDim.x + threadIdx.x;
+        if (p < L.n) out[off + p] = val[k];
+        if (NORM) v = norm_type == 2 ? fmax(v, fabs(val[k])) : v + val[k] * val[k];
     }
     if (NORM) {
         __shared__ double red[8];
-        double v = norm_type == 2 ? fabs(val) : val * val;
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) {
             const double o = __shfl_down_sync(FULL, v, d);
@@ -663,6 +708,213 @@ __global__ void __launch_bounds__(256) k_apply(LevelView L, const double* __rest
             double a = red[0];
             for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
                 a = norm_type == 2 ? fmax(a, red[w]) : a + red[w];
+            partials[(long)b * gridDim.x + blockIdx.x] = a;
+        }
+    }
+}
+
+// ------------------------------------------------------- tiled residual
+// One launch covers a level with two tile families: circle tiles (kTR
+// consecutive angles x kTS rings of the ring-major region, theta fast) and
+// radial tiles (kTR consecutive rows x kTS spokes of the spoke-major region,
+// r fast).  A tile stages u and the four coefficient arrays over the tile plus
+// a one-node halo (cross-region halo nodes are gathered from their NodeIndexing
+// position) with cp.async -- every load of the block is in flight at once --
+// then computes its rows from shared memory with fixed +-1 / +-kTW neighbour
+// offsets.  The across-origin phantom partner of ring 0 is read directly.
+constexpr int kTS = 8, kTR = 64, kTW = kTR + 2, kTH = (kTS + 2) * kTW;
+
+struct TileGeom {
+    int nca, ncr;  // circle tiles: angle tiles x ring tiles
+    int nrs, nrr;  // radial tiles: spoke tiles x row tiles
+    int ntiles() const { return nca * ncr + nrs * nrr; }
+};
+
+inline TileGeom tile_geom(const LevelView& L) {
+    TileGeom g;
+    g.nca = (L.nt + kTR - 1) / kTR;
+    g.ncr = (L.split + kTS - 1) / kTS;
+    g.nrs = L.len > 0 ? (L.nt + kTS - 1) / kTS : 0;
+    g.nrr = L.len > 0 ? (L.len + kTR - 1) / kTR : 0;
+    return g;
+}
+
+template <bool ONFLY, int MODE, bool NORM>
+__global__ void __launch_bounds__(256, 4) k_apply_tiled(LevelView L, TileGeom G,
+                                                        const double* __restrict__ u,
+                                                        const double* __restrict__ f,
+                                                        double* __restrict__ out,
+                                                        double* __restrict__ partials,
+                                                        int norm_type,
+                                                        const int* __restrict__ active) {
+    __shared__ double sU[kTH], sArr[kTH], sArt[kTH], sAtt[kTH], sDet[kTH], sF[kTS * kTR];
+    __shared__ double red[8];
+    const int b = blockIdx.y;
+    if (active && !active[b]) return;
+    const long off = (long)b * L.n;
+    const double* U = u + off;
+    const double* F = MODE == 0 ? nullptr : f + off;
+    const int N = L.nr - 1, nt = L.nt, len = L.len, split = L.split;
+    const int nct = G.nca * G.ncr;
+    const bool circ = (int)blockIdx.x < nct;
+    // tile origin: slow index (ring or spoke) and fast index (angle or row)
+    int slow0, fast0;
+    if (circ) {
+        slow0 = ((int)blockIdx.x / G.nca) * kTS;  // first ring
+        fast0 = ((int)blockIdx.x % G.nca) * kTR;  // first angle
+    } else {
+        const int tb = blockIdx.x - nct;
+        slow0 = (tb / G.nrr) * kTS;  // first spoke
+        fast0 = (tb % G.nrr) * kTR;  // first row (i = s - split)
+    }
+    // Per tile line j (slow index slow0 + j - 1): NodeIndexing base so that
+    // node k of the line (fast index fast0 + k - 1) is at base + k whenever k
+    // lies in [lo, hi]; nodes outside that range (cross-region halo, theta
+    // wrap) take the general index; invalid nodes (outside the level) are 0.
+    __shared__ long lBase[kTS + 2];
+    __shared__ int lLo[kTS + 2], lHi[kTS + 2], lS[kTS + 2], lT[kTS + 2];
+    if (threadIdx.x < kTS + 2) {
+        const int j = threadIdx.x;
+        if (circ) {
+            const int sl = slow0 + j - 1;
+            lS[j] = sl;
+            lT[j] = 0;
+            if (sl >= 0 && sl < split) {
+                lBase[j] = (long)sl * nt + fast0 - 1;  // node k -> angle fast0 + k - 1
+                lLo[j] = max(0, 1 - fast0);
+                lHi[j] = min(kTR + 1, nt - fast0);
+            } else {
+                lBase[j] = 0;
+                lLo[j] = 1;
+                lHi[j] = 0;  // empty: general path
+            }
+        } else {
+            int tl = slow0 + j - 1;
+            tl = ((tl % nt) + nt) % nt;
+            lS[j] = 0;
+            lT[j] = tl;
+            lBase[j] = (long)split * nt + (long)tl * len + fast0 - 1;  // node k -> row fast0+k-1
+            lLo[j] = max(0, 1 - fast0);
+            lHi[j] = min(kTR + 1, len - fast0);
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kTH; e += 256) {
+        const int j = e / kTW, k = e - j * kTW;  // k in [0, kTW): fast index fast0 + k - 1
+        int sv, tv;
+        bool ok;
+        long g;
+        if (circ) {
+            sv = lS[j];
+            tv = fast0 + k - 1;
+            if (tv < 0 || tv >= nt) tv = ((tv % nt) + nt) % nt;
+            ok = sv >= 0 && sv <= N;
+        } else {
+            tv = lT[j];
+            sv = split + fast0 + k - 1;
+            ok = sv <= N;
+        }
+        if (k >= lLo[j] && k <= lHi[j])
+            g = lBase[j] + k;
+        else
+            g = ok ? (long)L.idx(sv, tv) : 0;
+        if (ok) {
+            __pipeline_memcpy_async(&sU[e], U + g, 8);
+            if (ONFLY) {
+                const Coef c = transform(L.geo, L.alpha[(long)b * L.nr + sv], L.r[sv], L.sn[tv],
+                                         L.cs[tv], nullptr);
+                sArr[e] = c.arr;
+                sArt[e] = c.art;
+                sAtt[e] = c.att;
+                sDet[e] = c.det;
+            } else {
+                __pipeline_memcpy_async(&sArr[e], L.arr + off + g, 8);
+                __pipeline_memcpy_async(&sArt[e], L.art + off + g, 8);
+                __pipeline_memcpy_async(&sAtt[e], L.att + off + g, 8);
+                __pipeline_memcpy_async(&sDet[e], L.det + off + g, 8);
+            }
+            if (MODE == 1 && j >= 1 && j <= kTS && k >= 1 && k <= kTR)
+                __pipeline_memcpy_async(&sF[(j - 1) * kTR + (k - 1)], F + g, 8);
+        } else {
+            sU[e] = 0.0;
+            sArr[e] = sArt[e] = sAtt[e] = sDet[e] = 0.0;
+        }
+    }
+    __pipeline_commit();
+    __pipeline_wait_prior(0);
+    __syncthreads();
+    // neighbour strides in the tile: radial (s+-1) and angular (t+-1)
+    const int dS = circ ? kTW : 1, dT = circ ? 1 : kTW;
+    const int kk = threadIdx.x & (kTR - 1);
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int jj = (threadIdx.x >> 6) + 4 * q;
+        int s, t;
+        bool mine;
+        if (circ) {
+            s = slow0 + jj;
+            t = fast0 + kk;
+            mine = s < split && t < nt;
+        } else {
+            t = slow0 + jj;
+            s = split + fast0 + kk;
+            mine = t < nt && s <= N;
+        }
+        double val = 0.0;
+        if (mine) {
+            const int e = (jj + 1) * kTW + (kk + 1);
+            const double up = sU[e];
+            double acc = 0.0;
+            if (L.dir(s)) {
+                acc += 1.0 * up;
+            } else {
+                const int tm = t == 0 ? nt - 1 : t - 1;
+                const Coef cP = {sArr[e], sArt[e], sAtt[e], sDet[e]};
+                const Coef cTM = {sArr[e - dT], sArt[e - dT], sAtt[e - dT], sDet[e - dT]};
+                const Coef cTP = {sArr[e + dT], sArt[e + dT], sAtt[e + dT], sDet[e + dT]};
+                const Coef cSM = {sArr[e - dS], sArt[e - dS], sAtt[e - dS], sDet[e - dS]};
+                const Coef cSP = {sArr[e + dS], sArt[e + dS], sAtt[e + dS], sDet[e + dS]};
+                double anti = 0.0, uanti = 0.0;
+                if (s == 0 && L.boundary == 0) {  // phantom partner (0, t + nt/2)
+                    const int t2 = t + nt / 2 >= nt ? t + nt / 2 - nt : t + nt / 2;
+                    anti = ONFLY ? transform(L.geo, L.alpha[(long)b * L.nr], L.r[0], L.sn[t2],
+                                             L.cs[t2], nullptr).arr
+                                 : L.arr[off + t2];
+                    uanti = U[t2];
+                }
+                const Row R = row_from(L, b, s, t, tm, cP, cTM, cTP, cSM, cSP, anti);
+                acc += R.d * up;
+                if (R.has_sm) acc += R.sm * sU[e - dS];
+                if (R.has_sp) acc += R.sp * sU[e + dS];
+                acc += R.tm * sU[e - dT];
+                acc += R.tp * sU[e + dT];
+                if (R.has_sm) {
+                    acc += R.mm * sU[e - dS - dT];
+                    acc += R.mp * sU[e - dS + dT];
+                }
+                if (R.has_sp) {
+                    acc += R.pm * sU[e + dS - dT];
+                    acc += R.pp * sU[e + dS + dT];
+                }
+                if (R.origin) acc += R.ph * uanti;
+            }
+            val = MODE == 0 ? acc : sF[jj * kTR + kk] - acc;
+            out[off + L.idx(s, t)] = val;
+        }
+        if (NORM) v = norm_type == 2 ? fmax(v, fabs(val)) : v + val * val;
+    }
+    if (NORM) {
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            const double o = __shfl_down_sync(FULL, v, d);
+            v = norm_type == 2 ? fmax(v, o) : v + o;
+        }
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double a = red[0];
+            for (int w = 1; w < 8; ++w) a = norm_type == 2 ? fmax(a, red[w]) : a + red[w];
             partials[(long)b * gridDim.x + blockIdx.x] = a;
         }
     }
@@ -807,18 +1059,12 @@ __global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict_
 // ---------------------------------------------------------------- transfers
 // restrict_transpose (interpolation.cpp:97-143) fused with
 // mask_dirichlet_rows (multigrid.cpp:146-153) and the coarse u = 0 (:204).
-__global__ void __launch_bounds__(256) k_restrict(LevelView F, LevelView C, Weights w,
-                                                  const double* __restrict__ fr,
-                                                  double* __restrict__ cf,
-                                                  double* __restrict__ cu, int mask,
-                                                  const int* __restrict__ active) {
-    const int b = blockIdx.y;
-    if (active && !active[b]) return;
-    const int pc = blockIdx.x * blockDim.x + threadIdx.x;
-    if (pc >= C.n) return;
+__device__ __forceinline__ void restrict_node(const LevelView& F, const LevelView& C,
+                                              const Weights& w, const double* __restrict__ R,
+                                              double* __restrict__ cf, double* __restrict__ cu,
+                                              int mask, int pc) {
     int sc, tc;
     C.node(pc, sc, tc);
-    const double* R = fr + (long)b * F.n;
     const int sf = 2 * sc, tf = 2 * tc;
     const int tdn = tf == 0 ? F.nt - 1 : tf - 1;
     const int tup = tf + 1;
@@ -836,23 +1082,31 @@ __global__ void __launch_bounds__(256) k_restrict(LevelView F, LevelView C, Weig
         acc += w.rwb[sf + 1] * w.awb[tup] * R[F.idx(sf + 1, tup)];
     }
     if (mask && C.dir(sc)) acc = 0.0;
-    cf[(long)b * C.n + pc] = acc;
-    if (cu) cu[(long)b * C.n + pc] = 0.0;
+    cf[pc] = acc;
+    if (cu) cu[pc] = 0.0;
 }
 
-// prolongate(_add) (interpolation.cpp:38-95)
-template <bool ADD>
-__global__ void __launch_bounds__(256) k_prolong(LevelView F, LevelView C, Weights w,
-                                                 const double* __restrict__ cu,
-                                                 double* __restrict__ fu,
-                                                 const int* __restrict__ active) {
+// restrict_transpose (interpolation.cpp:97-143) fused with
+// mask_dirichlet_rows (multigrid.cpp:146-153) and the coarse u = 0 (:204).
+__global__ void __launch_bounds__(256) k_restrict(LevelView F, LevelView C, Weights w,
+                                                  const double* __restrict__ fr,
+                                                  double* __restrict__ cf,
+                                                  double* __restrict__ cu, int mask,
+                                                  const int* __restrict__ active) {
     const int b = blockIdx.y;
     if (active && !active[b]) return;
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= F.n) return;
+    const int pc = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pc >= C.n) return;
+    restrict_node(F, C, w, fr + (long)b * F.n, cf + (long)b * C.n,
+                  cu ? cu + (long)b * C.n : nullptr, mask, pc);
+}
+
+template <bool ADD>
+__device__ __forceinline__ void prolong_node(const LevelView& F, const LevelView& C,
+                                             const Weights& w, const double* __restrict__ X,
+                                             double* __restrict__ Y, int p) {
     int sf, tf;
     F.node(p, sf, tf);
-    const double* X = cu + (long)b * C.n;
     const bool ro = sf & 1, so = tf & 1;
     const int sc = sf >> 1, tc = tf >> 1;
     const int tcu = tc + 1 == C.nt ? 0 : tc + 1;
@@ -868,24 +1122,29 @@ __global__ void __launch_bounds__(256) k_prolong(LevelView F, LevelView C, Weigh
         v = wb * vb * X[C.idx(sc, tc)] + wb * va * X[C.idx(sc, tcu)] +
             wa * vb * X[C.idx(sc + 1, tc)] + wa * va * X[C.idx(sc + 1, tcu)];
     }
-    double* Y = fu + (long)b * F.n;
     if (ADD)
         Y[p] += v;
     else
         Y[p] = v;
 }
 
-// coarsest-level direct solve: u = f; envelope LDL^T solve
-// (multigrid.cpp:183-187, line_algebra.cpp:211-255), one thread per section.
-__global__ void k_coarse(EnvFactor E, const double* __restrict__ f, double* __restrict__ u,
-                         int B, const int* __restrict__ active) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= B || (active && !active[b])) return;
+// prolongate(_add) (interpolation.cpp:38-95)
+template <bool ADD>
+__global__ void __launch_bounds__(256) k_prolong(LevelView F, LevelView C, Weights w,
+                                                 const double* __restrict__ cu,
+                                                 double* __restrict__ fu,
+                                                 const int* __restrict__ active) {
+    const int b = blockIdx.y;
+    if (active && !active[b]) return;
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= F.n) return;
+    prolong_node<ADD>(F, C, w, cu + (long)b * C.n, fu + (long)b * F.n, p);
+}
+
+__device__ __forceinline__ void env_solve(const EnvFactor& E, int b, double* __restrict__ x) {
     const int n = E.n;
-    double* x = u + (long)b * n;
     const double* Lb = E.L + (long)b * E.nnz;
     const double* D = E.D + (long)b * n;
-    for (int i = 0; i < n; ++i) x[i] = f[(long)b * n + i];
     for (int i = 0; i < n; ++i) {
         const int fi = E.fc[i];
         const double* ri = Lb + E.ro[i] - fi;
@@ -900,6 +1159,504 @@ __global__ void k_coarse(EnvFactor E, const double* __restrict__ f, double* __re
         const double xi = x[i];
         for (int k = fi; k < i; ++k) x[k] -= ri[k] * xi;
     }
+}
+
+// coarsest-level direct solve: u = f; envelope LDL^T solve
+// (multigrid.cpp:183-187, line_algebra.cpp:211-255), one thread per section.
+__global__ void k_coarse(EnvFactor E, const double* __restrict__ f, double* __restrict__ u,
+                         int B, const int* __restrict__ active) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B || (active && !active[b])) return;
+    double* x = u + (long)b * E.n;
+    for (int i = 0; i < E.n; ++i) x[i] = f[(long)b * E.n + i];
+    env_solve(E, b, x);
+}
+
+// ------------------------------------------------------- coarse-level cycle
+// Below a size threshold every multigrid phase of a level is a few
+// microseconds of latency, so the whole sub-cycle of the coarse levels runs in
+// ONE launch: one block per section walks a host-generated op program
+// (smooth / residual / restrict / prolongate / coarsest solve, the exact
+// sequence of multigrid.cpp:189-220) with __syncthreads between phases.
+// Smoother lines are solved one per warp: each lane owns kWK consecutive rows,
+// the chunk carries are scanned with warp shuffles (no shared memory).
+constexpr int kWK = 8;  // rows per lane: lines up to 256 nodes
+
+template <int NV, bool FWD>
+__device__ __forceinline__ void warp_scan(double A, double (&B)[NV], double (&yin)[NV]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const double Ao = FWD ? __shfl_up_sync(FULL, A, d) : __shfl_down_sync(FULL, A, d);
+        double Bo[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+            Bo[v] = FWD ? __shfl_up_sync(FULL, B[v], d) : __shfl_down_sync(FULL, B[v], d);
+        if (FWD ? (lane >= d) : (lane + d < 32)) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) B[v] = A * Bo[v] + B[v];
+            A = A * Ao;
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        const double prev = FWD ? __shfl_up_sync(FULL, B[v], 1) : __shfl_down_sync(FULL, B[v], 1);
+        yin[v] = lane == (FWD ? 0 : 31) ? 0.0 : prev;
+    }
+}
+
+__device__ __forceinline__ void warp_scan2(Map2 a, bool fwd, double& in0, double& in1) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const Map2 o = shfl2(a, d, fwd);
+        if (fwd ? (lane >= d) : (lane + d < 32)) a = compose2(a, o);
+    }
+    const double q0 = fwd ? __shfl_up_sync(FULL, a.c0, 1) : __shfl_down_sync(FULL, a.c0, 1);
+    const double q1 = fwd ? __shfl_up_sync(FULL, a.c1, 1) : __shfl_down_sync(FULL, a.c1, 1);
+    const bool first = lane == (fwd ? 0 : 31);
+    in0 = first ? 0.0 : q0;
+    in1 = first ? 0.0 : q1;
+}
+
+// Warp solve of L L^T x = y (+ Sherman-Morrison when CYC); y[] holds the
+// lane's rows [lane*kWK, +kWK) on entry and the solution on exit.  Ld: raw L
+// diagonal, Mo: sub-diagonal, both global (this line).
+template <bool CYC>
+__device__ __forceinline__ void warp_line_solve(double (&y)[kWK], const double* __restrict__ Ld,
+                                                const double* __restrict__ Mo, int n,
+                                                double corner) {
+    constexpr int NV = CYC ? 2 : 1;
+    const int KE = (n + 31) >> 5;  // rows per lane (<= kWK)
+    const int j0 = (threadIdx.x & 31) * KE;
+    double il[kWK], mprev[kWK], z[CYC ? kWK : 1];
+    double A = 1.0, Bv[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) Bv[v] = 0.0;
+#pragma unroll
+    for (int q = 0; q < kWK; ++q) {
+        const int j = j0 + q;
+        const bool in = q < KE && j < n;
+        il[q] = in ? __drcp_rn(Ld[j]) : 0.0;
+        mprev[q] = (in && j > 0) ? Mo[j - 1] : 0.0;
+        if (in) {
+            const double a = -(mprev[q] * il[q]);
+            Bv[0] = a * Bv[0] + y[q] * il[q];
+            if (CYC) Bv[NV - 1] = a * Bv[NV - 1] + ((j == 0 || j == n - 1) ? il[q] : 0.0);
+            A = a * A;
+        }
+    }
+    double yin[NV];
+    warp_scan<NV, true>(A, Bv, yin);
+    double yp = yin[0], zp = yin[NV - 1];
+#pragma unroll
+    for (int q = 0; q < kWK; ++q) {
+        if (q < KE && j0 + q < n) {
+            yp = (y[q] - mprev[q] * yp) * il[q];
+            y[q] = yp;
+            if (CYC) {
+                const int j = j0 + q;
+                zp = (((j == 0 || j == n - 1) ? 1.0 : 0.0) - mprev[q] * zp) * il[q];
+                z[CYC ? q : 0] = zp;
+            }
+        }
+    }
+    double G = 1.0, Dv[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) Dv[v] = 0.0;
+    double mj[kWK];  // m_j couples row j to j+1
+#pragma unroll
+    for (int q = 0; q < kWK; ++q) {
+        const int j = j0 + q;
+        mj[q] = (q < KE && j < n - 1) ? Mo[j] : 0.0;
+    }
+#pragma unroll
+    for (int q = kWK - 1; q >= 0; --q) {
+        if (q < KE && j0 + q < n) {
+            const double g = -(mj[q] * il[q]);
+            Dv[0] = g * Dv[0] + y[q] * il[q];
+            if (CYC) Dv[NV - 1] = g * Dv[NV - 1] + z[CYC ? q : 0] * il[q];
+            G = g * G;
+        }
+    }
+    double xin[NV];
+    warp_scan<NV, false>(G, Dv, xin);
+    double xp = xin[0], zq = xin[NV - 1];
+#pragma unroll
+    for (int q = kWK - 1; q >= 0; --q) {
+        if (q < KE && j0 + q < n) {
+            xp = (y[q] - mj[q] * xp) * il[q];
+            y[q] = xp;
+            if (CYC) {
+                zq = (z[CYC ? q : 0] - mj[q] * zq) * il[q];
+                z[CYC ? q : 0] = zq;
+            }
+        }
+    }
+    if (CYC) {
+        // x_0, z_0 live on lane 0; x_{n-1}, z_{n-1} on lane (n-1)/kWK
+        const int last = (n - 1) / KE, ql = (n - 1) - last * KE;
+        double xl = 0.0, zl = 0.0;
+#pragma unroll
+        for (int q = 0; q < kWK; ++q)
+            if (q == ql) {
+                xl = y[q];
+                zl = z[CYC ? q : 0];
+            }
+        const double x0 = __shfl_sync(FULL, y[0], 0), z0 = __shfl_sync(FULL, z[0], 0);
+        xl = __shfl_sync(FULL, xl, last);
+        zl = __shfl_sync(FULL, zl, last);
+        const double tau = corner * (x0 + xl) / (1.0 + corner * (z0 + zl));
+#pragma unroll
+        for (int q = 0; q < kWK; ++q) y[q] -= tau * z[CYC ? q : 0];
+    }
+}
+
+
+// rhs of circle row (s,t): f - sum of the off-line couplings (smoother.cpp:162-182)
+template <bool ONFLY>
+__device__ __forceinline__ double circle_rhs(const LevelView& L, const double* __restrict__ U,
+                                             const double* __restrict__ F, long off, int b, int s,
+                                             int t) {
+    const int p = s * L.nt + t;
+    const CoefAt<ONFLY> cf{&L, off, b};
+    const Nbr q = neighbours(L, s, t, p);
+    const Row R = make_row_fast(L, cf, s, t, p, q);
+    double acc = F[p];
+    if (R.has_sm) acc -= R.sm * U[q.pSM];
+    if (R.has_sp) acc -= R.sp * U[q.pSP];
+    if (R.has_sm) {
+        acc -= R.mm * U[q.pSMTM];
+        acc -= R.mp * U[q.pSMTP];
+    }
+    if (R.has_sp) {
+        acc -= R.pm * U[q.pSPTM];
+        acc -= R.pp * U[q.pSPTP];
+    }
+    return acc;
+}
+
+// warp version of origin_solve (2nd-order recurrences as 2x2-map scans)
+template <bool ONFLY>
+__device__ void origin_warp(const CoarseLevel& C, double* __restrict__ U,
+                            const double* __restrict__ F, long off, int b) {
+    const LevelView& L = C.v;
+    const int n = L.nt, h = n / 2, nb = n - 2;
+    const int KE = (n + 31) >> 5;  // rows per lane (<= kWK)
+    const int lane = threadIdx.x & 31, j0 = lane * KE;
+    const long o = (long)b * n;
+    const double* b1 = C.of.band1 + o;
+    const double* b2 = C.of.band2 + o;
+    const double* r1 = C.of.row1 + o;
+    const double* r2 = C.of.row2 + o;
+    const double* D = C.of.D + o;
+    double x[kWK];
+    Map2 m = {1.0, 0.0, 0.0, 1.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < kWK; ++q) {
+        const int i = j0 + q;
+        const bool in = q < KE;
+        x[q] = (in && i < n) ? circle_rhs<ONFLY>(L, U, F, off, b, 0, operm(i, h)) : 0.0;
+        if (in && i < nb) {
+            const double l1 = i >= 1 ? b1[i] : 0.0, l2 = i >= 2 ? b2[i] : 0.0;
+            const Map2 mi = {0.0, 1.0, -l2, -l1, 0.0, x[q]};
+            m = compose2(mi, m);
+        }
+    }
+    double zm2, zm1;
+    warp_scan2(m, true, zm2, zm1);
+    double s1 = 0.0, s2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < kWK; ++q) {
+        const int i = j0 + q;
+        if (q < KE && i < nb) {
+            double sum = x[q];
+            if (i >= 2) sum -= b2[i] * zm2;
+            if (i >= 1) sum -= b1[i] * zm1;
+            x[q] = sum;
+            zm2 = zm1;
+            zm1 = sum;
+            if (i >= C.of.fc1) s1 += r1[i] * sum;
+            if (i >= C.of.fc2) s2 += r2[i] * sum;
+        }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        s1 += __shfl_xor_sync(FULL, s1, d);
+        s2 += __shfl_xor_sync(FULL, s2, d);
+    }
+    double xr2 = 0.0, xr1 = 0.0;  // rhs of the closing rows n-2, n-1
+#pragma unroll
+    for (int q = 0; q < kWK; ++q) {
+        if (q < KE && j0 + q == n - 2) xr2 = x[q];
+        if (q < KE && j0 + q == n - 1) xr1 = x[q];
+    }
+    xr2 = __shfl_sync(FULL, xr2, (n - 2) / KE);
+    xr1 = __shfl_sync(FULL, xr1, (n - 1) / KE);
+    const double zn2 = xr2 - s1;
+    double zn1 = xr1 - s2;
+    if (n - 2 >= C.of.fc2) zn1 -= r2[n - 2] * zn2;
+    const double xn1 = zn1 / D[n - 1];
+    double xn2 = zn2 / D[n - 2];
+    if (n - 2 >= C.of.fc2) xn2 -= r2[n - 2] * xn1;
+    Map2 g = {1.0, 0.0, 0.0, 1.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = kWK - 1; q >= 0; --q) {
+        const int k = j0 + q;
+        if (q < KE && k < nb) {
+            double gk = x[q] / D[k];
+            if (k >= C.of.fc2) gk -= r2[k] * xn1;
+            if (k >= C.of.fc1) gk -= r1[k] * xn2;
+            x[q] = gk;
+            const double l1 = k + 1 < nb ? b1[k + 1] : 0.0;
+            const double l2 = k + 2 < nb ? b2[k + 2] : 0.0;
+            const Map2 mk = {-l1, -l2, 1.0, 0.0, gk, 0.0};
+            g = compose2(mk, g);
+        }
+    }
+    double xp1, xp2;
+    warp_scan2(g, false, xp1, xp2);
+#pragma unroll
+    for (int q = kWK - 1; q >= 0; --q) {
+        const int k = j0 + q;
+        if (q < KE && k < nb) {
+            double xv = x[q];
+            if (k + 2 < nb) xv -= b2[k + 2] * xp2;
+            if (k + 1 < nb) xv -= b1[k + 1] * xp1;
+            x[q] = xv;
+            xp2 = xp1;
+            xp1 = xv;
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < kWK; ++q) {
+        const int k = j0 + q;
+        if (q >= KE) continue;
+        if (k < nb) U[operm(k, h)] = x[q];
+        if (k == n - 2) U[operm(k, h)] = xn2;
+        if (k == n - 1) U[operm(k, h)] = xn1;
+    }
+}
+
+template <bool ONFLY>
+__device__ void coarse_smooth(const CoarseLevel& C, int b) {
+    const LevelView& L = C.v;
+    const long off = (long)b * L.n;
+    double* U = C.u + off;
+    const double* F = C.f + off;
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+    const int nt = L.nt;
+    for (int parity = 0; parity < 2; ++parity) {  // circle sweeps (smoother.cpp:95-116)
+        const int lines = L.split > parity ? (L.split - parity + 1) / 2 : 0;
+        for (int li = warp; li < lines; li += nw) {
+            const int s = parity + 2 * li;
+            if (L.dir(s)) {
+                for (int t = lane; t < nt; t += 32) U[s * nt + t] = F[s * nt + t];
+                continue;
+            }
+            if (s == 0 && L.boundary == 0) {
+                origin_warp<ONFLY>(C, U, F, off, b);
+                continue;
+            }
+            double y[kWK];
+            const int KE = (nt + 31) >> 5;
+            const int j0 = lane * KE;
+#pragma unroll
+            for (int q = 0; q < kWK; ++q)
+                y[q] = (q < KE && j0 + q < nt) ? circle_rhs<ONFLY>(L, U, F, off, b, s, j0 + q) : 0.0;
+            const long fo = (long)b * L.split * nt + (long)s * nt;
+            warp_line_solve<true>(y, C.cl + fo, C.cm + fo, nt, C.corner[(long)b * L.split + s]);
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < kWK; ++q)
+                if (q < KE && j0 + q < nt) U[s * nt + j0 + q] = y[q];
+        }
+        __syncthreads();
+    }
+    if (L.len <= 0) return;
+    const CoefAt<ONFLY> cf{&L, off, b};
+    for (int parity = 0; parity < 2; ++parity) {  // radial sweeps (smoother.cpp:118-142)
+        const int lines = (nt - parity + 1) / 2;
+        for (int li = warp; li < lines; li += nw) {
+            const int t = parity + 2 * li;
+            const int base = L.split * nt + t * L.len;
+            double y[kWK];
+            const int KE = (L.len + 31) >> 5;
+            const int j0 = lane * KE;
+#pragma unroll
+            for (int q = 0; q < kWK; ++q) {
+                const int i = j0 + q, s = L.split + i;
+                double acc = 0.0;
+                if (q < KE && i < L.len) {
+                    const int p = base + i;
+                    if (L.dir(s)) {
+                        acc = F[p];
+                    } else {
+                        const Nbr nb = neighbours(L, s, t, p);
+                        const Row R = make_row_fast(L, cf, s, t, p, nb);
+                        acc = F[p];
+                        if (s == L.split && R.has_sm) acc -= R.sm * U[nb.pSM];
+                        acc -= R.tm * U[nb.pTM];
+                        acc -= R.tp * U[nb.pTP];
+                        if (R.has_sm) {
+                            acc -= R.mm * U[nb.pSMTM];
+                            acc -= R.mp * U[nb.pSMTP];
+                        }
+                        if (R.has_sp) {
+                            acc -= R.pm * U[nb.pSPTM];
+                            acc -= R.pp * U[nb.pSPTP];
+                        }
+                    }
+                }
+                y[q] = acc;
+            }
+            const long fo = ((long)b * nt + t) * L.len;
+            warp_line_solve<false>(y, C.rl + fo, C.rm + fo, L.len, 0.0);
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < kWK; ++q)
+                if (q < KE && j0 + q < L.len) U[base + j0 + q] = y[q];
+        }
+        __syncthreads();
+    }
+}
+
+template <class T>
+__device__ __forceinline__ T* rebase_ptr(T* p, char* base) {
+    const uintptr_t o = reinterpret_cast<uintptr_t>(p);
+    return o == 0 ? nullptr : reinterpret_cast<T*>(base + (o - 8));
+}
+
+__device__ void rebase_level(CoarseLevel& c, char* base) {
+    LevelView& v = c.v;
+    v.r = rebase_ptr(v.r, base);
+    v.h = rebase_ptr(v.h, base);
+    v.k = rebase_ptr(v.k, base);
+    v.sn = rebase_ptr(v.sn, base);
+    v.cs = rebase_ptr(v.cs, base);
+    v.alpha = rebase_ptr(v.alpha, base);
+    v.beta = rebase_ptr(v.beta, base);
+    v.arr = rebase_ptr(v.arr, base);
+    v.art = rebase_ptr(v.art, base);
+    v.att = rebase_ptr(v.att, base);
+    v.det = rebase_ptr(v.det, base);
+    v.rh = rebase_ptr(v.rh, base);
+    v.rk = rebase_ptr(v.rk, base);
+    v.B = 1;
+    c.u = rebase_ptr(c.u, base);
+    c.f = rebase_ptr(c.f, base);
+    c.res = rebase_ptr(c.res, base);
+    c.cl = rebase_ptr(c.cl, base);
+    c.cm = rebase_ptr(c.cm, base);
+    c.corner = rebase_ptr(c.corner, base);
+    c.rl = rebase_ptr(c.rl, base);
+    c.rm = rebase_ptr(c.rm, base);
+    c.of.band1 = rebase_ptr(c.of.band1, base);
+    c.of.band2 = rebase_ptr(c.of.band2, base);
+    c.of.row1 = rebase_ptr(c.of.row1, base);
+    c.of.row2 = rebase_ptr(c.of.row2, base);
+    c.of.D = rebase_ptr(c.of.D, base);
+    c.w.rwb = rebase_ptr(c.w.rwb, base);
+    c.w.rwa = rebase_ptr(c.w.rwa, base);
+    c.w.awb = rebase_ptr(c.w.awb, base);
+    c.w.awa = rebase_ptr(c.w.awa, base);
+}
+
+// Executes the op program; `bb` is the section index used for per-section
+// arrays (0 when the data is shared-memory resident and section-sliced).
+template <bool ONFLY>
+__device__ __forceinline__ void run_prog(const CoarseLevel* lv, const EnvFactor& env,
+                                         const int* __restrict__ prog, int nops, int bb) {
+    for (int i = 0; i < nops; ++i) {
+        const int op = prog[i] & 255, l = prog[i] >> 8;
+        const CoarseLevel& C = lv[l];
+        const long off = (long)bb * C.v.n;
+        switch (op) {
+            case OP_SMOOTH:
+                coarse_smooth<ONFLY>(C, bb);
+                break;
+            case OP_RESIDUAL:
+                for (int p = threadIdx.x; p < C.v.n; p += blockDim.x)
+                    C.res[off + p] = apply_node<ONFLY, 1>(C.v, C.u + off, C.f + off, off, bb, p);
+                break;
+            case OP_RESTRICT: {
+                const CoarseLevel& D = lv[l + 1];
+                const long offc = (long)bb * D.v.n;
+                for (int p = threadIdx.x; p < D.v.n; p += blockDim.x)
+                    restrict_node(C.v, D.v, C.w, C.res + off, D.f + offc, D.u + offc, 1, p);
+                break;
+            }
+            case OP_PROLONG: {
+                const CoarseLevel& D = lv[l + 1];
+                const long offc = (long)bb * D.v.n;
+                for (int p = threadIdx.x; p < C.v.n; p += blockDim.x)
+                    prolong_node<true>(C.v, D.v, C.w, D.u + offc, C.u + off, p);
+                break;
+            }
+            default: {  // OP_COARSE: u = f, envelope LDL^T (multigrid.cpp:183-187)
+                if (threadIdx.x == 0) {
+                    double* x = C.u + off;
+                    for (int k = 0; k < env.n; ++k) x[k] = C.f[off + k];
+                    env_solve(env, bb, x);
+                }
+                break;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <bool ONFLY>
+__global__ void __launch_bounds__(512) k_coarse_cycle(const __grid_constant__ CoarseParams cp,
+                                                      const int* __restrict__ prog, int nops,
+                                                      const int* __restrict__ active) {
+    extern __shared__ __align__(16) char sbuf[];
+    __shared__ CoarseLevel slv[kMaxCoarse];
+    __shared__ EnvFactor senv;
+    const int b = blockIdx.x;
+    if (active && !active[b]) return;
+    if (!cp.resident) {
+        run_prog<ONFLY>(cp.lv - cp.first, cp.env, prog, nops, b);
+        return;
+    }
+    // stage this section's slice of every tail array into shared memory: warps
+    // take descriptors round-robin and issue asynchronous copies, one wait
+    {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+        for (int c = warp; c < cp.ncopy; c += nw) {
+            const CopyDesc d = cp.copies[c];
+            const char* src = static_cast<const char*>(d.src) + (long)b * d.stride;
+            const int words = d.bytes >> 3;
+            for (int w = lane; w < words; w += 32)
+                __pipeline_memcpy_async(sbuf + d.dst + 8 * w, src + 8 * w, 8);
+            if ((d.bytes & 7) && lane == 0)  // int arrays of odd length
+                __pipeline_memcpy_async(sbuf + d.dst + (d.bytes - 4), src + (d.bytes - 4), 4);
+        }
+        __pipeline_commit();
+        __pipeline_wait_prior(0);
+    }
+    const int nl = cp.lv[0].v.nr == 0 ? 0 : kMaxCoarse;
+    if (threadIdx.x < kMaxCoarse) {
+        CoarseLevel c = cp.lv[threadIdx.x];
+        if (c.v.nr > 0) rebase_level(c, sbuf);
+        slv[threadIdx.x] = c;
+    }
+    if (threadIdx.x == 0) {
+        EnvFactor e = cp.env;
+        e.fc = rebase_ptr(e.fc, sbuf);
+        e.ro = rebase_ptr(e.ro, sbuf);
+        e.L = rebase_ptr(e.L, sbuf);
+        e.D = rebase_ptr(e.D, sbuf);
+        senv = e;
+    }
+    (void)nl;
+    __syncthreads();
+    run_prog<ONFLY>(slv - cp.first, senv, prog, nops, 0);
+    // the top level's correction goes back to global memory
+    const CoarseLevel& top = slv[0];
+    for (int p = threadIdx.x; p < top.v.n; p += blockDim.x)
+        cp.top_u_global[(long)b * top.v.n + p] = top.u[p];
 }
 
 // ------------------------------------------------------------------- norms
@@ -1018,7 +1775,11 @@ void set_smem(KernelT kern, size_t bytes) {
     const auto key = std::make_pair(reinterpret_cast<const void*>(kern), dev);
     std::lock_guard<std::mutex> lock(mu);
     if (done.count(key)) return;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncAttributes fa;
+    int optin = 227 * 1024;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess) optin -= (int)fa.sharedSizeBytes;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     done.insert(key);
 }
 
@@ -1040,16 +1801,19 @@ inline size_t line_smem(int n) { return (size_t)(3 * padded(n) + 32 * 6 + 16) * 
 
 }  // namespace
 
-int apply_blocks(const LevelView& L) { return (L.n + 255) / 256; }
+int apply_launches(const LevelView& L) { return 1; }
+
+int apply_blocks(const LevelView& L) { return tile_geom(L).ntiles(); }
 
 int launch_apply(const LevelView& L, bool onfly, int mode, const double* u, const double* f,
                  double* out, double* partials, int norm_type, const int* active,
                  cudaStream_t st) {
-    const int nb = apply_blocks(L);
+    const TileGeom G = tile_geom(L);
+    const int nb = G.ntiles();
     dim3 grid(nb, L.B);
     const bool norm = partials != nullptr;
 #define PMG_APPLY(ON, MO, NO) \
-    k_apply<ON, MO, NO><<<grid, 256, 0, st>>>(L, u, f, out, partials, norm_type, active)
+    k_apply_tiled<ON, MO, NO><<<grid, 256, 0, st>>>(L, G, u, f, out, partials, norm_type, active)
     if (onfly) {
         if (mode == 0) {
             if (norm) PMG_APPLY(true, 0, true); else PMG_APPLY(true, 0, false);
@@ -1183,4 +1947,18 @@ void launch_flush(double* buf, long n, cudaStream_t st) {
     k_flush<<<148 * 8, 256, 0, st>>>(buf, n);
 }
 
+}  // namespace pmg
+
+namespace pmg {
+void launch_coarse_cycle(const CoarseParams& cp, const int* prog, int nops, int B, bool onfly,
+                         const int* active, cudaStream_t st) {
+    const size_t sm = cp.resident ? (size_t)cp.smem_bytes : 0;
+    if (onfly) {
+        set_smem(k_coarse_cycle<true>, sm);
+        k_coarse_cycle<true><<<B, 512, sm, st>>>(cp, prog, nops, active);
+    } else {
+        set_smem(k_coarse_cycle<false>, sm);
+        k_coarse_cycle<false><<<B, 512, sm, st>>>(cp, prog, nops, active);
+    }
+}
 }  // namespace pmg

@@ -36,6 +36,47 @@ struct Weights {  // transfer weights of a fine level (interpolation.cpp:19-36)
     const double* awa;  // [nt] angular_weight_above(tf)
 };
 
+// Device description of one level for the single-launch coarse cycle.
+struct CoarseLevel {
+    LevelView v;
+    double *u, *f, *res;
+    const double *cl, *cm, *corner;  // circle factors [B][split*nt], corner [B][split]
+    const double *rl, *rm;           // radial factors [B][nt*len]
+    OriginFactor of;
+    Weights w;  // this level as the fine level of a transfer
+};
+
+enum CoarseOp { OP_SMOOTH = 0, OP_RESIDUAL = 1, OP_RESTRICT = 2, OP_PROLONG = 3, OP_COARSE = 4 };
+
+// Level descriptors of the coarse tail passed BY VALUE (constant bank):
+// lv[i] describes level first + i.
+constexpr int kMaxCoarse = 12;
+// One array of one level copied into shared memory (resident tail).
+struct CopyDesc {
+    const void* src;  // global base of section 0
+    long stride;      // bytes between sections (0: shared by all sections)
+    int bytes;        // bytes to copy
+    int dst;          // byte offset in dynamic shared memory
+};
+struct CoarseParams {
+    CoarseLevel lv[kMaxCoarse];
+    EnvFactor env;
+    int first;
+    // resident mode: every pointer above holds (shared-memory byte offset + 8),
+    // 0 = null; the block copies `ncopy` arrays in, runs, and writes the top
+    // level's u back to `top_u_global`
+    int resident;
+    int ncopy;
+    int smem_bytes;
+    const CopyDesc* copies;
+    double* top_u_global;
+};
+
+// Runs an op program (op | level << 8) over the coarse levels, one block per
+// section.
+void launch_coarse_cycle(const CoarseParams& cp, const int* prog, int nops, int B, bool onfly,
+                         const int* active, cudaStream_t st);
+
 // kernel classes for launch accounting / profiling
 enum KernelKind {
     KK_RESIDUAL = 0,
@@ -57,6 +98,7 @@ int launch_apply(const LevelView& L, bool onfly, int mode, const double* u, cons
                  double* out, double* partials, int norm_type, const int* active,
                  cudaStream_t st);
 int apply_blocks(const LevelView& L);
+int apply_launches(const LevelView& L);  // kernels one launch_apply issues
 
 // serial: line solves in the reference's sequential operation order (bitwise
 // reproduction of the reference); otherwise chunked parallel scans.

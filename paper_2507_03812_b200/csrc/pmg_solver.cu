@@ -204,6 +204,11 @@ struct Solver {
     double *norms = nullptr, *partials = nullptr, *r0 = nullptr, *hist = nullptr;
     int *active = nullptr, *iters = nullptr, *conv = nullptr, *remaining = nullptr;
     int* count = nullptr;
+    // single-launch coarse tail: levels >= coarse_start run in k_coarse_cycle
+    int coarse_start = -1;
+    CoarseParams coarse_params{};
+    int* d_prog[3] = {nullptr, nullptr, nullptr};
+    int prog_len[3] = {0, 0, 0};
     // CUDA graph of one cycle + residual norm + convergence check
     cudaGraphExec_t cycle_exec = nullptr;
     long long cycle_nodes = 0;
@@ -329,6 +334,7 @@ struct Solver {
             V.g = std::move(grids[l]);
             setup_level(V, l == L - 1, bad);
         }
+        setup_coarse_tail();
         // convergence state
         hist_cap = std::max(set.max_iterations, 0) + 1;
         norms = alloc<double>(B);
@@ -451,6 +457,160 @@ struct Solver {
             setup_weights(V);
         } else {
             setup_coarsest(V);
+        }
+    }
+
+    // op program of cycle(l, type) (multigrid.cpp:189-220) for k_coarse_cycle
+    void gen_prog(int l, int type, std::vector<int>& prog) const {
+        const int L = static_cast<int>(lv.size());
+        if (l == L - 1) {
+            prog.push_back(OP_COARSE | (l << 8));
+            return;
+        }
+        for (int i = 0; i < set.pre_smoothing; ++i) prog.push_back(OP_SMOOTH | (l << 8));
+        prog.push_back(OP_RESIDUAL | (l << 8));
+        prog.push_back(OP_RESTRICT | (l << 8));
+        if (type == 0) {
+            gen_prog(l + 1, 0, prog);
+        } else if (type == 1) {
+            gen_prog(l + 1, 1, prog);
+            gen_prog(l + 1, 1, prog);
+        } else {
+            gen_prog(l + 1, 2, prog);
+            gen_prog(l + 1, 0, prog);
+        }
+        prog.push_back(OP_PROLONG | (l << 8));
+        for (int i = 0; i < set.post_smoothing; ++i) prog.push_back(OP_SMOOTH | (l << 8));
+    }
+
+    // Levels qualify for the single-block coarse tail when every line fits a
+    // warp (<= 32*kWK nodes).  Resident mode (default): the tail is the largest
+    // set of coarsest levels whose per-section data fits the shared-memory
+    // budget; the block stages it into shared memory and runs the whole
+    // sub-cycle there.
+    void setup_coarse_tail() {
+        const int L = static_cast<int>(lv.size());
+        if (serial) return;  // reference_order needs the exact-order level kernels
+        long budget = 200 * 1024;
+        if (const char* e = std::getenv("PMG_COARSE_SMEM")) budget = std::atol(e);
+        if (budget <= 0) return;
+        auto fits_warp = [&](int l) {
+            const HostGrid& g = lv[l].g;
+            return g.nt() <= 32 * 8 && (g.nr() - g.split) <= 32 * 8 && g.uniform_angles;
+        };
+        // bytes of one section's slice of level l in the resident tail
+        auto level_bytes = [&](int l, bool top) {
+            const HostGrid& g = lv[l].g;
+            const long n = g.n(), nr = g.nr(), nt = g.nt(), sp = g.split, len = nr - sp;
+            const bool coarsest = l == L - 1;
+            long d = 2 * nr + 6 * nt + 2 * nr;     // r, h, rh, k, sn, cs, rk(+pad), alpha, beta
+            if (!onfly) d += 4 * n;                 // arr art att det
+            d += 2 * n;                             // u, f
+            if (!coarsest) {
+                d += n;                             // res
+                d += 2 * sp * nt + sp + 2 * nt * len + 5 * nt + 2 * nr + 2 * nt;
+            } else {
+                d += lv[l].env.nnz + n + n / 2 + n + 2;  // L, D, fc (ints), ro (longs)
+            }
+            (void)top;
+            return d * 8 + 40 * 16;                 // + alignment slack
+        };
+        int start = L;
+        long total = 0;
+        for (int l = L - 1; l >= 0; --l) {
+            if (!fits_warp(l) && l != L - 1) break;
+            const long bl = level_bytes(l, true);
+            if (total + bl > budget) break;
+            total += bl;
+            start = l;
+        }
+        if (L - start > kMaxCoarse) start = L - kMaxCoarse;
+        if (start >= L - 1) return;  // only the coarsest: nothing to gain
+        coarse_start = start;
+        std::memset(&coarse_params, 0, sizeof coarse_params);
+        coarse_params.first = start;
+        std::vector<CopyDesc> plan;
+        long off = 0;
+        // allocate `count` elements of `esz` bytes at a 16-byte aligned offset;
+        // copy from src (stride = per-section bytes, 0 = shared) if src != null
+        auto place = [&](const void* src, long stride, long count, int esz) -> void* {
+            off = (off + 15) & ~15L;
+            const long at = off;
+            off += count * esz;
+            if (src) plan.push_back(CopyDesc{src, stride, static_cast<int>(count * esz),
+                                             static_cast<int>(at)});
+            return reinterpret_cast<void*>(at + 8);
+        };
+        for (int l = start; l < L; ++l) {
+            Level& V = lv[l];
+            const HostGrid& g = V.g;
+            const long n = g.n(), nr = g.nr(), nt = g.nt(), sp = g.split, len = nr - sp;
+            const bool coarsest = l == L - 1, top = l == start;
+            CoarseLevel& c = coarse_params.lv[l - start];
+            c.v = V.v;
+            LevelView& v = c.v;
+            v.r = static_cast<double*>(place(V.v.r, 0, nr, 8));
+            v.h = static_cast<double*>(place(V.v.h, 0, nr - 1, 8));
+            v.rh = static_cast<double*>(place(V.v.rh, 0, nr - 1, 8));
+            v.k = static_cast<double*>(place(V.v.k, 0, nt, 8));
+            v.rk = static_cast<double*>(place(V.v.rk, 0, nt, 8));
+            v.sn = static_cast<double*>(place(V.v.sn, 0, nt, 8));
+            v.cs = static_cast<double*>(place(V.v.cs, 0, nt, 8));
+            v.alpha = static_cast<double*>(place(V.v.alpha, nr * 8, nr, 8));
+            v.beta = static_cast<double*>(place(V.v.beta, nr * 8, nr, 8));
+            if (!onfly) {
+                v.arr = static_cast<double*>(place(V.v.arr, n * 8, n, 8));
+                v.art = static_cast<double*>(place(V.v.art, n * 8, n, 8));
+                v.att = static_cast<double*>(place(V.v.att, n * 8, n, 8));
+                v.det = static_cast<double*>(place(V.v.det, n * 8, n, 8));
+            }
+            c.u = static_cast<double*>(place(top ? V.u : nullptr, n * 8, n, 8));
+            c.f = static_cast<double*>(place(top ? V.f : nullptr, n * 8, n, 8));
+            if (!coarsest) {
+                c.res = static_cast<double*>(place(nullptr, 0, n, 8));
+                c.cl = static_cast<double*>(place(V.cil, sp * nt * 8, sp * nt, 8));
+                c.cm = static_cast<double*>(place(V.cm, sp * nt * 8, sp * nt, 8));
+                c.corner = static_cast<double*>(place(V.corner, sp * 8, sp, 8));
+                if (len > 0) {
+                    c.rl = static_cast<double*>(place(V.ril, nt * len * 8, nt * len, 8));
+                    c.rm = static_cast<double*>(place(V.rm, nt * len * 8, nt * len, 8));
+                }
+                if (set.boundary_mode == 0) {
+                    c.of.band1 = static_cast<double*>(place(V.ob1, nt * 8, nt, 8));
+                    c.of.band2 = static_cast<double*>(place(V.ob2, nt * 8, nt, 8));
+                    c.of.row1 = static_cast<double*>(place(V.or1, nt * 8, nt, 8));
+                    c.of.row2 = static_cast<double*>(place(V.or2, nt * 8, nt, 8));
+                    c.of.D = static_cast<double*>(place(V.oD, nt * 8, nt, 8));
+                    c.of.fc1 = V.ofc1;
+                    c.of.fc2 = V.ofc2;
+                }
+                c.w.rwb = static_cast<double*>(place(V.w.rwb, 0, nr, 8));
+                c.w.rwa = static_cast<double*>(place(V.w.rwa, 0, nr, 8));
+                c.w.awb = static_cast<double*>(place(V.w.awb, 0, nt, 8));
+                c.w.awa = static_cast<double*>(place(V.w.awa, 0, nt, 8));
+            } else {
+                const EnvFactor& E = V.env;
+                coarse_params.env = E;
+                coarse_params.env.fc = static_cast<int*>(place(E.fc, 0, E.n, 4));
+                coarse_params.env.ro = static_cast<long*>(place(E.ro, 0, E.n + 1, 8));
+                coarse_params.env.L = static_cast<double*>(place(E.L, E.nnz * 8, E.nnz, 8));
+                coarse_params.env.D = static_cast<double*>(place(E.D, E.n * 8, E.n, 8));
+            }
+        }
+        if (off > 220 * 1024) {  // budget estimate too small: stay non-resident
+            coarse_start = -1;
+            return;
+        }
+        coarse_params.resident = 1;
+        coarse_params.ncopy = static_cast<int>(plan.size());
+        coarse_params.smem_bytes = static_cast<int>((off + 15) & ~15L);
+        coarse_params.copies = upload(plan);
+        coarse_params.top_u_global = lv[start].u;
+        for (int type = 0; type < 3; ++type) {
+            std::vector<int> prog;
+            gen_prog(start, type, prog);
+            d_prog[type] = upload(prog);
+            prog_len[type] = static_cast<int>(prog.size());
         }
     }
 
@@ -594,7 +754,7 @@ struct Solver {
     }
     void residual(int l, const int* act) {
         Level& V = lv[l];
-        run(KK_RESIDUAL, 1, [&] {
+        run(KK_RESIDUAL, apply_launches(V.v), [&] {
             launch_apply(V.v, onfly, 1, V.u, V.f, V.res, nullptr, 0, act, stream);
         });
     }
@@ -616,6 +776,13 @@ struct Solver {
     // multigrid.cpp:189-220
     void cycle(int l, int type, const int* act) {
         const int L = static_cast<int>(lv.size());
+        if (l == coarse_start) {
+            run(KK_COARSE, 1, [&] {
+                launch_coarse_cycle(coarse_params, d_prog[type], prog_len[type], B, onfly, act,
+                                    stream);
+            });
+            return;
+        }
         if (l == L - 1) {
             coarse(l, act);
             return;
@@ -640,7 +807,7 @@ struct Solver {
     void norm_check() {
         Level& V = lv[0];
         int nb = 0;
-        run(KK_RESIDUAL, 1, [&] {
+        run(KK_RESIDUAL, apply_launches(V.v), [&] {
             nb = launch_apply(V.v, onfly, 1, V.u, V.f, V.res, partials, set.norm_type, active,
                               stream);
         });
@@ -1057,7 +1224,7 @@ int pmg_seeded_rhs(pmg_handle h, unsigned seed, double* ustar_host, int layout) 
             for (int t = 0; t < g.nt(); ++t) ub[g.idx(g.nr() - 1, t)] = 0.0;
         }
         s.h2d(V.res, us.data(), (long)us.size());
-        s.run(pmg::KK_RESIDUAL, 1, [&] {
+        s.run(pmg::KK_RESIDUAL, pmg::apply_launches(V.v), [&] {
             pmg::launch_apply(V.v, s.onfly, 0, V.res, nullptr, V.f, nullptr, 0, nullptr,
                               s.stream);
         });
@@ -1100,7 +1267,7 @@ int pmg_apply(pmg_handle h, int level, const double* u, double* y) {
         pmg::Level& V = s.lv[level];
         const long N = (long)s.B * V.v.n;
         s.h2d(V.u, u, N);
-        s.run(pmg::KK_RESIDUAL, 1, [&] {
+        s.run(pmg::KK_RESIDUAL, pmg::apply_launches(V.v), [&] {
             pmg::launch_apply(V.v, s.onfly, 0, V.u, nullptr, V.res, nullptr, 0, nullptr,
                               s.stream);
         });
