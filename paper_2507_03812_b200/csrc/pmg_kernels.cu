@@ -1021,10 +1021,53 @@ __global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict_
     const CoefAt<ONFLY> cf{&L, off, b};
     const long fo = ((long)b * L.nt + t) * len;
     for (int i = threadIdx.x; i < len; i += T) {
-        const int s = split + i;
         const double lv = ril[fo + i];
         IL[P(i)] = serial ? lv : __drcp_rn(lv);
         M[P(i)] = rm[fo + i];
+    }
+    // interior rows split < s < n_r-1 (Take): only the off-line couplings --
+    // angular (att) and corner (art) -- with direct spoke-major offsets; all
+    // operands of two rows are loaded before any arithmetic (memory-level
+    // parallelism).  Same expressions as row_from, so bitwise identical.
+    int ifirst = 1, ilast = len - 2;  // rows 0 (s = split) and len-1 (s = n_r-1) below
+    if (!ONFLY) {
+        const int tm = L.tminus(t), tp = L.tplus(t);
+        const double km = L.k[tm], kp = L.k[t], rkm = L.rk[tm], rkp = L.rk[t];
+        const int dTM = (tm - t) * len, dTP = (tp - t) * len;
+        const double* __restrict__ ATT = L.att + off;
+        const double* __restrict__ ART = L.art + off;
+        const int N = L.nr - 1;
+#pragma unroll 2
+        for (int i = ifirst + threadIdx.x; i <= ilast; i += T) {
+            const int s = split + i, p = base + i;
+            const double fP = F[p];
+            const double attP = ATT[p], attM = ATT[p + dTM], attQ = ATT[p + dTP];
+            const double artM = ART[p + dTM], artQ = ART[p + dTP];
+            const double artSM = ART[p - 1], artSP = ART[p + 1];
+            const double uM = U[p + dTM], uQ = U[p + dTP];
+            const double uMM = U[p + dTM - 1], uQM = U[p + dTP - 1];
+            const double uMP = U[p + dTM + 1], uQP = U[p + dTP + 1];
+            const double hbar = 0.5 * (L.h[s - 1] + L.h[s]);
+            const double south = -xdiv(hbar, km, rkm) * (attP + attM);
+            const double north = -xdiv(hbar, kp, rkp) * (attP + attQ);
+            double acc = fP;
+            acc -= south * uM;
+            acc -= north * uQ;
+            acc -= (-(artM + artSM) * 0.25) * uMM;
+            acc -= ((artSM + artQ) * 0.25) * uQM;
+            if (s + 1 < N || !L.dir(s + 1)) {  // coupling to ring s+1 kept
+                acc -= ((artM + artSP) * 0.25) * uMP;
+                acc -= (-(artSP + artQ) * 0.25) * uQP;
+            }
+            Y[P(i)] = acc;
+        }
+    } else {
+        ifirst = len;  // Give: the general path below handles every row
+        ilast = -1;
+    }
+    for (int i = threadIdx.x; i < len; i += T) {
+        if (i >= ifirst && i <= ilast) continue;
+        const int s = split + i;
         const int p = base + i;
         if (L.dir(s)) {
             Y[P(i)] = F[p];
