@@ -342,8 +342,8 @@ def run_gpu(args):
                    key=lambda k: breakdown.get(k, {"ms": 0})["ms"])
 
     # ---- roofline of the dominant kernel on the finest level
-    roof = kernel_roofline(solver, dominant, peak, peak_kind, reps=20)
-    kernels = {k: kernel_roofline(solver, k, peak, peak_kind, reps=20)
+    roof = kernel_roofline(solver, dominant, peak, peak_kind, reps=20, workload=args.workload)
+    kernels = {k: kernel_roofline(solver, k, peak, peak_kind, reps=20, workload=args.workload)
                for k in ("residual", "circle", "radial")}
 
     if rank != 0:
@@ -392,7 +392,17 @@ def run_gpu(args):
     return 0
 
 
-def kernel_roofline(solver, kind, peak, peak_kind, reps=20):
+def ncu_traffic(workload, kind):
+    """DRAM bytes per launch (B+W pair for sweeps) of the finest-level kernel
+    from the committed ncu capture (profiles/ncu_traffic.json), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh).get(workload, {}).get(kind)
+    except Exception:
+        return None
+
+
+def kernel_roofline(solver, kind, peak, peak_kind, reps=20, workload=None):
     """achieved = algorithmic bytes per launch / CUDA-event time per launch on
     the finest level (L2 flushed before every repetition)."""
     nr, nt, split = solver.level_shape(0)
@@ -410,7 +420,8 @@ def kernel_roofline(solver, kind, peak, peak_kind, reps=20):
     gbs = algo / (ms * 1e-3) / 1e9
     return {"kernel": f"{kind} (finest level{', B+W' if kind != 'residual' else ''})",
             "bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(gbs / peak, 4), "traffic": None, "ms_per_launch": round(ms, 5),
+            "frac": round(gbs / peak, 4), "traffic": ncu_traffic(workload, kind),
+            "ms_per_launch": round(ms, 5),
             "algorithmic_bytes": algo, "bytes_per_node": BYTES_PER_NODE[kind],
             "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"}
 
@@ -430,7 +441,7 @@ def run_c4(args, rank, world, local, stream, peak, peak_kind, dist):
     reps = args.reps
     out = {}
     for k in ("residual", "circle", "radial"):
-        out[k] = kernel_roofline(solver, k, peak, peak_kind, reps=reps)
+        out[k] = kernel_roofline(solver, k, peak, peak_kind, reps=reps, workload="c4")
     if rank == 0:
         line = {"metric": "smoother/residual HBM GB/s (config 4 microbench)",
                 "value": out["radial"]["achieved"], "unit": "GB/s", "n_gpus": world,
