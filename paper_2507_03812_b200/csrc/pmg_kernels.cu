@@ -10,8 +10,11 @@
 //
 // All arrays carry a leading section dimension [B][...]; blockIdx.y is the
 // section, and sections whose `active` flag is 0 (converged) are skipped.
+#include <cooperative_groups.h>
 #include <cuda_pipeline.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <set>
 #include <utility>
@@ -19,6 +22,8 @@
 #include "pmg_kernels.h"
 
 namespace pmg {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -1099,6 +1104,387 @@ __global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict_
     for (int i = threadIdx.x; i < len; i += T) U[base + i] = Y[P(i)];
 }
 
+// ------------------------------------------------- cluster-split line solves
+// A long smoother line is split over a thread-block cluster of C CTAs (rows
+// [r*R, r*R+R) on rank r).  Each CTA scans its chunk carries in-block
+// (block_scan_ex), then the CTA composites are composed across the cluster
+// through distributed shared memory, so shared memory per CTA shrinks by C and
+// several lines run per SM (the single-CTA line kernels hold one 6889-row
+// line per SM at 8193x8192).
+
+// Block scan returning, per thread, the exclusive prefix map (Aex, Bex) of the
+// earlier chunks of this CTA (scan order) and the CTA total (At, Bt).
+template <int NV, bool FWD>
+__device__ __forceinline__ void block_scan_ex(double A, double (&B)[NV], double& Aex,
+                                              double (&Bex)[NV], double& At, double (&Bt)[NV],
+                                              double* scr) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const double Ao = FWD ? __shfl_up_sync(FULL, A, d) : __shfl_down_sync(FULL, A, d);
+        double Bo[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+            Bo[v] = FWD ? __shfl_up_sync(FULL, B[v], d) : __shfl_down_sync(FULL, B[v], d);
+        if (FWD ? (lane >= d) : (lane + d < 32)) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) B[v] = A * Bo[v] + B[v];
+            A = A * Ao;
+        }
+    }
+    if (lane == (FWD ? 31 : 0)) {
+        scr[warp * (NV + 1)] = A;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) scr[warp * (NV + 1) + 1 + v] = B[v];
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const int wi = FWD ? lane : nw - 1 - lane;
+        double a = 1.0, bb[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) bb[v] = 0.0;
+        if (lane < nw) {
+            a = scr[wi * (NV + 1)];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) bb[v] = scr[wi * (NV + 1) + 1 + v];
+        }
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double ao = __shfl_up_sync(FULL, a, d);
+            double bo[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) bo[v] = __shfl_up_sync(FULL, bb[v], d);
+            if (lane >= d) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v) bb[v] = a * bo[v] + bb[v];
+                a = a * ao;
+            }
+        }
+        if (lane < nw) {
+            scr[wi * (NV + 1)] = a;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) scr[wi * (NV + 1) + 1 + v] = bb[v];
+        }
+    }
+    __syncthreads();
+    const int pw = FWD ? warp - 1 : warp + 1;
+    double pA = 1.0, pB[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) pB[v] = 0.0;
+    if (pw >= 0 && pw < nw) {
+        pA = scr[pw * (NV + 1)];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) pB[v] = scr[pw * (NV + 1) + 1 + v];
+    }
+    const double fA = A * pA;
+    const double qa = FWD ? __shfl_up_sync(FULL, fA, 1) : __shfl_down_sync(FULL, fA, 1);
+    const bool first = lane == (FWD ? 0 : 31);
+    Aex = first ? pA : qa;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        const double fB = A * pB[v] + B[v];
+        const double qb = FWD ? __shfl_up_sync(FULL, fB, 1) : __shfl_down_sync(FULL, fB, 1);
+        Bex[v] = first ? pB[v] : qb;
+    }
+    const int last = FWD ? nw - 1 : 0;  // last warp in scan order holds the CTA total
+    At = scr[last * (NV + 1)];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) Bt[v] = scr[last * (NV + 1) + 1 + v];
+    __syncthreads();
+}
+
+// Carry entering this CTA: the CTA totals of the earlier ranks (scan order)
+// composed and applied to 0.  xch: this CTA's NV+1 exchange slots.
+template <int NV, bool FWD>
+__device__ __forceinline__ void cluster_carry(double At, const double (&Bt)[NV], double* xch,
+                                              double (&carry)[NV]) {
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = cl.block_rank(), C = cl.num_blocks();
+    if (threadIdx.x == 0) {
+        xch[0] = At;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) xch[1 + v] = Bt[v];
+    }
+    cl.sync();
+#pragma unroll
+    for (int v = 0; v < NV; ++v) carry[v] = 0.0;
+    if (FWD) {
+        for (int r = 0; r < rank; ++r) {
+            const double* x = cl.map_shared_rank(xch, r);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) carry[v] = x[0] * carry[v] + x[1 + v];
+        }
+    } else {
+        for (int r = C - 1; r > rank; --r) {
+            const double* x = cl.map_shared_rank(xch, r);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) carry[v] = x[0] * carry[v] + x[1 + v];
+        }
+    }
+    cl.sync();  // remote reads done before the slots are reused
+}
+
+// Solve of rows [row0, row0+nloc) of an ntot-row LL^T (+ SM) line held by a
+// cluster.  Y: local rhs in / x out; IL: 1/l; Mx[P(j)] = m_{row0+j-1}
+// (j = 0..nloc; 0 before global row 0).  xch: 8 doubles of exchange space.
+template <int K, bool CYC>
+__device__ __forceinline__ void line_solve_cl(double* Y, const double* IL, const double* Mx,
+                                              int nloc, int row0, int ntot, double corner,
+                                              double* scr, double* xch) {
+    constexpr int NV = CYC ? 2 : 1;
+    const int j0 = threadIdx.x * K;
+    double y[K], z[CYC ? K : 1];
+    double A = 1.0, Bv[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) Bv[v] = 0.0;
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+        const int j = j0 + q, g = row0 + j;
+        if (j < nloc) {
+            const double il = IL[P(j)];
+            const double a = g > 0 ? -(Mx[P(j)] * il) : 0.0;
+            const double b = Y[P(j)];
+            y[q] = b;
+            Bv[0] = a * Bv[0] + b * il;
+            if (CYC) Bv[NV - 1] = a * Bv[NV - 1] + ((g == 0 || g == ntot - 1) ? il : 0.0);
+            A = a * A;
+        }
+    }
+    double Aex, Bex[NV], At, Bt[NV], carry[NV];
+    block_scan_ex<NV, true>(A, Bv, Aex, Bex, At, Bt, scr);
+    cluster_carry<NV, true>(At, Bt, xch, carry);
+    {
+        double yp = Aex * carry[0] + Bex[0], zp = Aex * carry[NV - 1] + Bex[NV - 1];
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+            const int j = j0 + q, g = row0 + j;
+            if (j < nloc) {
+                const double il = IL[P(j)];
+                const double mp = g > 0 ? Mx[P(j)] : 0.0;
+                yp = (y[q] - mp * yp) * il;
+                y[q] = yp;
+                if (CYC) {
+                    zp = (((g == 0 || g == ntot - 1) ? 1.0 : 0.0) - mp * zp) * il;
+                    z[CYC ? q : 0] = zp;
+                }
+            }
+        }
+    }
+    double G = 1.0, Dv[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) Dv[v] = 0.0;
+#pragma unroll
+    for (int q = K - 1; q >= 0; --q) {
+        const int j = j0 + q, g = row0 + j;
+        if (j < nloc) {
+            const double il = IL[P(j)];
+            const double gg = g < ntot - 1 ? -(Mx[P(j + 1)] * il) : 0.0;
+            Dv[0] = gg * Dv[0] + y[q] * il;
+            if (CYC) Dv[NV - 1] = gg * Dv[NV - 1] + z[CYC ? q : 0] * il;
+            G = gg * G;
+        }
+    }
+    block_scan_ex<NV, false>(G, Dv, Aex, Bex, At, Bt, scr);
+    cluster_carry<NV, false>(At, Bt, xch, carry);
+    {
+        double xp = Aex * carry[0] + Bex[0], zq = Aex * carry[NV - 1] + Bex[NV - 1];
+#pragma unroll
+        for (int q = K - 1; q >= 0; --q) {
+            const int j = j0 + q, g = row0 + j;
+            if (j < nloc) {
+                const double il = IL[P(j)];
+                const double mj = g < ntot - 1 ? Mx[P(j + 1)] : 0.0;
+                xp = (y[q] - mj * xp) * il;
+                y[q] = xp;
+                if (CYC) {
+                    zq = (z[CYC ? q : 0] - mj * zq) * il;
+                    z[CYC ? q : 0] = zq;
+                }
+            }
+        }
+    }
+    if (CYC) {
+        // x, z at global rows 0 (rank 0) and ntot-1 (last rank), via DSMEM
+        cg::cluster_group cl = cg::this_cluster();
+        const int rank = cl.block_rank(), C = cl.num_blocks();
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+            const int j = j0 + q, g = row0 + j;
+            if (j < nloc && g == 0) {
+                xch[4] = y[q];
+                xch[5] = z[CYC ? q : 0];
+            }
+            if (j < nloc && g == ntot - 1) {
+                xch[6] = y[q];
+                xch[7] = z[CYC ? q : 0];
+            }
+        }
+        cl.sync();
+        const double* x0 = cl.map_shared_rank(xch, 0);
+        const double* xl = cl.map_shared_rank(xch, C - 1);
+        const double tau = corner * (x0[4] + xl[6]) / (1.0 + corner * (x0[5] + xl[7]));
+        (void)rank;
+        cl.sync();
+#pragma unroll
+        for (int q = 0; q < K; ++q) y[q] -= tau * z[CYC ? q : 0];
+    }
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+        const int j = j0 + q;
+        if (j < nloc) Y[P(j)] = y[q];
+    }
+    __syncthreads();
+}
+
+inline __device__ int cl_rows(int n, int C) {  // rows per CTA
+    return (n + C - 1) / C;
+}
+
+// Radial sweep with each spoke split over a cluster (fast mode, Take).
+template <int K>
+__global__ void __launch_bounds__(256) k_radial_cl(LevelView L, double* __restrict__ u,
+                                                   const double* __restrict__ f,
+                                                   const double* __restrict__ ril,
+                                                   const double* __restrict__ rm, int parity,
+                                                   const int* __restrict__ active) {
+    extern __shared__ double smem[];
+    __shared__ double xch[8];
+    cg::cluster_group cl = cg::this_cluster();
+    const int C = cl.num_blocks(), rank = cl.block_rank();
+    const int b = blockIdx.y;
+    if (active && !active[b]) return;
+    const int t = parity + 2 * (blockIdx.x / C);
+    const int len = L.len, split = L.split, T = blockDim.x;
+    const int R = cl_rows(len, C), row0 = rank * R;
+    const int nloc = min(R, len - row0);
+    const long off = (long)b * L.n;
+    double* U = u + off;
+    const double* F = f + off;
+    const int base = split * L.nt + t * len;
+    const int pn = padded(R + 1);
+    double* Y = smem;
+    double* IL = smem + pn;
+    double* Mx = IL + pn;
+    double* scr = Mx + pn;
+    const long fo = ((long)b * L.nt + t) * len;
+    for (int j = threadIdx.x; j < nloc; j += T) IL[P(j)] = __drcp_rn(ril[fo + row0 + j]);
+    for (int j = threadIdx.x; j <= nloc; j += T)
+        Mx[P(j)] = row0 + j > 0 ? rm[fo + row0 + j - 1] : 0.0;
+    const int tm = L.tminus(t), tp = L.tplus(t);
+    const double km = L.k[tm], kp = L.k[t], rkm = L.rk[tm], rkp = L.rk[t];
+    const int dTM = (tm - t) * len, dTP = (tp - t) * len;
+    const double* __restrict__ ATT = L.att + off;
+    const double* __restrict__ ART = L.art + off;
+    const int N = L.nr - 1;
+    const CoefAt<false> cf{&L, off, b};
+#pragma unroll 2
+    for (int j = threadIdx.x; j < nloc; j += T) {
+        const int i = row0 + j, s = split + i, p = base + i;
+        double acc;
+        if (i > 0 && s < N) {
+            const double fP = F[p];
+            const double attP = ATT[p], attM = ATT[p + dTM], attQ = ATT[p + dTP];
+            const double artM = ART[p + dTM], artQ = ART[p + dTP];
+            const double artSM = ART[p - 1], artSP = ART[p + 1];
+            const double uM = U[p + dTM], uQ = U[p + dTP];
+            const double uMM = U[p + dTM - 1], uQM = U[p + dTP - 1];
+            const double uMP = U[p + dTM + 1], uQP = U[p + dTP + 1];
+            const double hbar = 0.5 * (L.h[s - 1] + L.h[s]);
+            const double south = -xdiv(hbar, km, rkm) * (attP + attM);
+            const double north = -xdiv(hbar, kp, rkp) * (attP + attQ);
+            acc = fP;
+            acc -= south * uM;
+            acc -= north * uQ;
+            acc -= (-(artM + artSM) * 0.25) * uMM;
+            acc -= ((artSM + artQ) * 0.25) * uQM;
+            if (s + 1 < N || !L.dir(s + 1)) {
+                acc -= ((artM + artSP) * 0.25) * uMP;
+                acc -= (-(artSP + artQ) * 0.25) * uQP;
+            }
+        } else if (L.dir(s)) {
+            acc = F[p];
+        } else {
+            const Nbr q = neighbours(L, s, t, p);
+            const Row R2 = make_row_fast(L, cf, s, t, p, q);
+            acc = F[p];
+            if (s == split && R2.has_sm) acc -= R2.sm * U[q.pSM];
+            acc -= R2.tm * U[q.pTM];
+            acc -= R2.tp * U[q.pTP];
+            if (R2.has_sm) {
+                acc -= R2.mm * U[q.pSMTM];
+                acc -= R2.mp * U[q.pSMTP];
+            }
+            if (R2.has_sp) {
+                acc -= R2.pm * U[q.pSPTM];
+                acc -= R2.pp * U[q.pSPTP];
+            }
+        }
+        Y[P(j)] = acc;
+    }
+    __syncthreads();
+    line_solve_cl<K, false>(Y, IL, Mx, nloc, row0, len, 0.0, scr, xch);
+    for (int j = threadIdx.x; j < nloc; j += T) U[base + row0 + j] = Y[P(j)];
+}
+
+// Circle sweep with each ring split over a cluster (fast mode); rings
+// s = s_first + 2*line; the across-origin ring is launched separately.
+template <bool ONFLY, int K>
+__global__ void __launch_bounds__(256) k_circle_cl(LevelView L, double* __restrict__ u,
+                                                   const double* __restrict__ f,
+                                                   const double* __restrict__ cil,
+                                                   const double* __restrict__ cm,
+                                                   const double* __restrict__ corner, int s_first,
+                                                   const int* __restrict__ active) {
+    extern __shared__ double smem[];
+    __shared__ double xch[8];
+    cg::cluster_group cl = cg::this_cluster();
+    const int C = cl.num_blocks(), rank = cl.block_rank();
+    const int b = blockIdx.y;
+    if (active && !active[b]) return;
+    const int s = s_first + 2 * (blockIdx.x / C);
+    const int nt = L.nt, T = blockDim.x;
+    const int R = cl_rows(nt, C), row0 = rank * R;
+    const int nloc = min(R, nt - row0);
+    const long off = (long)b * L.n;
+    double* U = u + off;
+    const double* F = f + off;
+    const int base = s * nt;
+    if (L.dir(s)) {
+        for (int j = threadIdx.x; j < nloc; j += T) U[base + row0 + j] = F[base + row0 + j];
+        return;
+    }
+    const int pn = padded(R + 1);
+    double* Y = smem;
+    double* IL = smem + pn;
+    double* Mx = IL + pn;
+    double* scr = Mx + pn;
+    const long fo = (long)b * L.split * nt + (long)s * nt;
+    for (int j = threadIdx.x; j < nloc; j += T) IL[P(j)] = __drcp_rn(cil[fo + row0 + j]);
+    for (int j = threadIdx.x; j <= nloc; j += T)
+        Mx[P(j)] = row0 + j > 0 ? cm[fo + row0 + j - 1] : 0.0;
+    const CoefAt<ONFLY> cf{&L, off, b};
+    for (int j = threadIdx.x; j < nloc; j += T) {
+        const int t = row0 + j, p = base + t;
+        const Nbr q = neighbours(L, s, t, p);
+        const Row R2 = make_row_fast(L, cf, s, t, p, q);
+        double acc = F[p];
+        if (R2.has_sm) acc -= R2.sm * U[q.pSM];
+        if (R2.has_sp) acc -= R2.sp * U[q.pSP];
+        if (R2.has_sm) {
+            acc -= R2.mm * U[q.pSMTM];
+            acc -= R2.mp * U[q.pSMTP];
+        }
+        if (R2.has_sp) {
+            acc -= R2.pm * U[q.pSPTM];
+            acc -= R2.pp * U[q.pSPTP];
+        }
+        Y[P(j)] = acc;
+    }
+    __syncthreads();
+    line_solve_cl<K, true>(Y, IL, Mx, nloc, row0, nt, corner[(long)b * L.split + s], scr, xch);
+    for (int j = threadIdx.x; j < nloc; j += T) U[base + row0 + j] = Y[P(j)];
+}
+
 // ---------------------------------------------------------------- transfers
 // restrict_transpose (interpolation.cpp:97-143) fused with
 // mask_dirichlet_rows (multigrid.cpp:146-153) and the coarse u = 0 (:204).
@@ -1885,13 +2271,135 @@ static void circle_k(const LevelView& L, double* u, const double* f, const doubl
                                                       serial ? 1 : 0, exact_rings, active);
 }
 
+// cluster size for a line of n rows in fast mode (1 = single-CTA kernels)
+static int line_cluster(int n, int min_rows = 2048) {
+    if (const char* e = std::getenv("PMG_CIRCLE_CLUSTER_ROWS")) {
+        const int rows = std::atoi(e);
+        if (rows <= 0) return 1;
+        return std::min(8, std::max(1, (n + rows - 1) / rows));
+    }
+    if (n < min_rows) return 1;
+    return std::min(8, (n + 2047) / 2048);
+}
+
+template <class Kern, class... Args>
+static void launch_cluster(Kern kern, int C, dim3 grid, int T, size_t smem, cudaStream_t st,
+                           Args... args) {
+    set_smem(kern, smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(T, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+static void cl_shape(int n, int C, int& R, int& K, int& T, size_t& smem) {
+    R = (n + C - 1) / C;
+    K = R <= 2048 ? 8 : 16;
+    T = (((R + K - 1) / K) + 31) / 32 * 32;
+    smem = (size_t)(3 * padded(R + 1) + 32 * 3 + 16) * sizeof(double);
+}
+
+int line_launches(const LevelView& L, bool serial, bool onfly, int exact_rings, int kind,
+                  int parity) {
+    if (kind == 0) {
+        const bool cl = !serial && exact_rings <= 0 && line_cluster(L.nt) > 1;
+        return (cl && parity == 0 && L.boundary == 0) ? 2 : 1;
+    }
+    return 1;
+}
+
 void launch_circle(const LevelView& L, bool onfly, double* u, const double* f, const double* cil,
                    const double* cm, const double* corner, const double* cz,
                    const OriginFactor& of, int parity, bool serial, int exact_rings,
                    const int* active, cudaStream_t st) {
     const int lines = L.split > parity ? (L.split - parity + 1) / 2 : 0;
     if (lines == 0) return;
+    const int C = (!serial && exact_rings <= 0) ? line_cluster(L.nt) : 1;
     int K, T;
+    if (C > 1) {
+        int s_first = parity, nl = lines;
+        // the across-origin ring runs as a single-CTA kernel on a side stream,
+        // forked from / joined back into st so it overlaps the clustered rings
+        // (a parallel branch when captured into the cycle graph)
+        cudaStream_t side = st;
+        cudaEvent_t fork = nullptr, join = nullptr;
+        if (parity == 0 && L.boundary == 0) {
+            static thread_local cudaStream_t s_side[64] = {};
+            static thread_local cudaEvent_t s_fork[64] = {}, s_join[64] = {};
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (!s_side[dev]) {
+                cudaStreamCreateWithFlags(&s_side[dev], cudaStreamNonBlocking);
+                cudaEventCreateWithFlags(&s_fork[dev], cudaEventDisableTiming);
+                cudaEventCreateWithFlags(&s_join[dev], cudaEventDisableTiming);
+            }
+            side = s_side[dev];
+            fork = s_fork[dev];
+            join = s_join[dev];
+            cudaEventRecord(fork, st);
+            cudaStreamWaitEvent(side, fork, 0);
+        }
+        if (parity == 0 && L.boundary == 0) {  // across-origin ring: single-CTA kernel
+            line_shape(L.nt, K, T);
+            const size_t sm = line_smem(L.nt);
+#define PMG_C1(KK)                                                                               \
+    do {                                                                                         \
+        if (onfly) {                                                                             \
+            set_smem(k_circle<true, KK>, sm);                                                    \
+            k_circle<true, KK><<<dim3(1, L.B), T, sm, side>>>(L, u, f, cil, cm, corner, cz, of, 0, \
+                                                              0, 0, active);                     \
+        } else {                                                                                 \
+            set_smem(k_circle<false, KK>, sm);                                                   \
+            k_circle<false, KK><<<dim3(1, L.B), T, sm, side>>>(L, u, f, cil, cm, corner, cz, of, \
+                                                               0, 0, 0, active);                 \
+        }                                                                                        \
+    } while (0)
+            switch (K) {
+                case 2: PMG_C1(2); break;
+                case 4: PMG_C1(4); break;
+                case 8: PMG_C1(8); break;
+                default: PMG_C1(16); break;
+            }
+#undef PMG_C1
+            s_first = 2;
+            nl = L.split > 2 ? (L.split - 2 + 1) / 2 : 0;
+        }
+        if (nl > 0) {
+            int R;
+            size_t sm;
+            cl_shape(L.nt, C, R, K, T, sm);
+            const dim3 grid(nl * C, L.B);
+            if (K == 8) {
+                if (onfly)
+                    launch_cluster(k_circle_cl<true, 8>, C, grid, T, sm, st, L, u, f, cil, cm,
+                                   corner, s_first, active);
+                else
+                    launch_cluster(k_circle_cl<false, 8>, C, grid, T, sm, st, L, u, f, cil, cm,
+                                   corner, s_first, active);
+            } else {
+                if (onfly)
+                    launch_cluster(k_circle_cl<true, 16>, C, grid, T, sm, st, L, u, f, cil, cm,
+                                   corner, s_first, active);
+                else
+                    launch_cluster(k_circle_cl<false, 16>, C, grid, T, sm, st, L, u, f, cil, cm,
+                                   corner, s_first, active);
+            }
+        }
+        if (join) {
+            cudaEventRecord(join, side);
+            cudaStreamWaitEvent(st, join, 0);
+        }
+        return;
+    }
     line_shape(L.nt, K, T);
 #define PMG_C(KK)                                                                            \
     (onfly ? circle_k<true, KK>(L, u, f, cil, cm, corner, cz, of, parity, serial, exact_rings, \
@@ -1923,6 +2431,22 @@ void launch_radial(const LevelView& L, bool onfly, double* u, const double* f, c
     if (L.len <= 0) return;
     const int lines = (L.nt - parity + 1) / 2;
     int K, T;
+    if (!serial && !onfly && L.len > 1024) {
+        int C = std::min(8, (L.len + 899) / 900);
+        if (const char* e = std::getenv("PMG_LINE_CLUSTER_ROWS")) {
+            const int rows = std::atoi(e);
+            if (rows > 0) C = std::min(8, std::max(1, (L.len + rows - 1) / rows));
+        }
+        int R;
+        size_t sm;
+        cl_shape(L.len, C, R, K, T, sm);
+        const dim3 grid(lines * C, L.B);
+        if (K == 8)
+            launch_cluster(k_radial_cl<8>, C, grid, T, sm, st, L, u, f, ril, rm, parity, active);
+        else
+            launch_cluster(k_radial_cl<16>, C, grid, T, sm, st, L, u, f, ril, rm, parity, active);
+        return;
+    }
     line_shape(L.len, K, T);
 #define PMG_R(KK)                                                                       \
     (onfly ? radial_k<true, KK>(L, u, f, ril, rm, parity, serial, active, st, T, lines) \

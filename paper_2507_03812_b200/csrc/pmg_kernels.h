@@ -108,6 +108,9 @@ void launch_circle(const LevelView& L, bool onfly, double* u, const double* f, c
                    const double* cm, const double* corner, const double* cz,
                    const OriginFactor& of, int parity, bool serial, int exact_rings,
                    const int* active, cudaStream_t st);
+// kernels one launch_circle (kind 0) / launch_radial (kind 1) issues
+int line_launches(const LevelView& L, bool serial, bool onfly, int exact_rings, int kind,
+                  int parity);
 void launch_radial(const LevelView& L, bool onfly, double* u, const double* f, const double* ril,
                    const double* rm, int parity, bool serial, const int* active,
                    cudaStream_t st);

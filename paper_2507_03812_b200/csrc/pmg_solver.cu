@@ -742,7 +742,7 @@ struct Solver {
     void smooth(int l, const int* act) {
         Level& V = lv[l];
         for (int parity = 0; parity < 2; ++parity)
-            run(KK_CIRCLE, 1, [&] {
+            run(KK_CIRCLE, line_launches(V.v, serial, onfly, exact_rings, 0, parity), [&] {
                 launch_circle(V.v, onfly, V.u, V.f, V.cil, V.cm, V.corner, V.cz, V.of(), parity,
                               serial, exact_rings, act, stream);
             });
