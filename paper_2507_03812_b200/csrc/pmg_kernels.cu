@@ -2301,9 +2301,9 @@ static void launch_cluster(Kern kern, int C, dim3 grid, int T, size_t smem, cuda
     cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-static void cl_shape(int n, int C, int& R, int& K, int& T, size_t& smem) {
+static void cl_shape(int n, int C, int& R, int& K, int& T, size_t& smem, int kpref = 8) {
     R = (n + C - 1) / C;
-    K = R <= 2048 ? 8 : 16;
+    K = R <= 1024 && kpref == 4 ? 4 : (R <= 2048 ? 8 : 16);
     T = (((R + K - 1) / K) + 31) / 32 * 32;
     smem = (size_t)(3 * padded(R + 1) + 32 * 3 + 16) * sizeof(double);
 }
@@ -2439,9 +2439,13 @@ void launch_radial(const LevelView& L, bool onfly, double* u, const double* f, c
         }
         int R;
         size_t sm;
-        cl_shape(L.len, C, R, K, T, sm);
+        int kp = 8;
+        if (const char* e = std::getenv("PMG_RADIAL_K")) kp = std::atoi(e);
+        cl_shape(L.len, C, R, K, T, sm, kp);
         const dim3 grid(lines * C, L.B);
-        if (K == 8)
+        if (K == 4)
+            launch_cluster(k_radial_cl<4>, C, grid, T, sm, st, L, u, f, ril, rm, parity, active);
+        else if (K == 8)
             launch_cluster(k_radial_cl<8>, C, grid, T, sm, st, L, u, f, ril, rm, parity, active);
         else
             launch_cluster(k_radial_cl<16>, C, grid, T, sm, st, L, u, f, ril, rm, parity, active);
