@@ -1609,7 +1609,9 @@ __global__ void k_coarse(EnvFactor E, const double* __restrict__ f, double* __re
 // sequence of multigrid.cpp:189-220) with __syncthreads between phases.
 // Smoother lines are solved one per warp: each lane owns kWK consecutive rows,
 // the chunk carries are scanned with warp shuffles (no shared memory).
-constexpr int kWK = 8;  // rows per lane: lines up to 256 nodes
+// KW = rows per lane (1, 2, 4 or 8: lines up to 32*KW nodes) is a template
+// parameter so the kernel carries only the code of its own line length (the
+// one-block tail is instruction-fetch bound when the code is large).
 
 template <int NV, bool FWD>
 __device__ __forceinline__ void warp_scan(double A, double (&B)[NV], double (&yin)[NV]) {
@@ -1649,21 +1651,21 @@ __device__ __forceinline__ void warp_scan2(Map2 a, bool fwd, double& in0, double
 }
 
 // Warp solve of L L^T x = y (+ Sherman-Morrison when CYC); y[] holds the
-// lane's rows [lane*kWK, +kWK) on entry and the solution on exit.  Ld: raw L
+// lane's rows [lane*KW, +KW) on entry and the solution on exit.  Ld: raw L
 // diagonal, Mo: sub-diagonal, both global (this line).
-template <bool CYC>
-__device__ __forceinline__ void warp_line_solve(double (&y)[kWK], const double* __restrict__ Ld,
+template <bool CYC, int KW>
+__device__ __forceinline__ void warp_line_solve(double (&y)[KW], const double* __restrict__ Ld,
                                                 const double* __restrict__ Mo, int n,
                                                 double corner) {
     constexpr int NV = CYC ? 2 : 1;
-    const int KE = (n + 31) >> 5;  // rows per lane (<= kWK)
+    const int KE = (n + 31) >> 5;  // rows per lane (<= KW)
     const int j0 = (threadIdx.x & 31) * KE;
-    double il[kWK], mprev[kWK], z[CYC ? kWK : 1];
+    double il[KW], mprev[KW], z[CYC ? KW : 1];
     double A = 1.0, Bv[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) Bv[v] = 0.0;
 #pragma unroll
-    for (int q = 0; q < kWK; ++q) {
+    for (int q = 0; q < KW; ++q) {
         const int j = j0 + q;
         const bool in = q < KE && j < n;
         il[q] = in ? __drcp_rn(Ld[j]) : 0.0;
@@ -1679,7 +1681,7 @@ __device__ __forceinline__ void warp_line_solve(double (&y)[kWK], const double* 
     warp_scan<NV, true>(A, Bv, yin);
     double yp = yin[0], zp = yin[NV - 1];
 #pragma unroll
-    for (int q = 0; q < kWK; ++q) {
+    for (int q = 0; q < KW; ++q) {
         if (q < KE && j0 + q < n) {
             yp = (y[q] - mprev[q] * yp) * il[q];
             y[q] = yp;
@@ -1693,14 +1695,14 @@ __device__ __forceinline__ void warp_line_solve(double (&y)[kWK], const double* 
     double G = 1.0, Dv[NV];
 #pragma unroll
     for (int v = 0; v < NV; ++v) Dv[v] = 0.0;
-    double mj[kWK];  // m_j couples row j to j+1
+    double mj[KW];  // m_j couples row j to j+1
 #pragma unroll
-    for (int q = 0; q < kWK; ++q) {
+    for (int q = 0; q < KW; ++q) {
         const int j = j0 + q;
         mj[q] = (q < KE && j < n - 1) ? Mo[j] : 0.0;
     }
 #pragma unroll
-    for (int q = kWK - 1; q >= 0; --q) {
+    for (int q = KW - 1; q >= 0; --q) {
         if (q < KE && j0 + q < n) {
             const double g = -(mj[q] * il[q]);
             Dv[0] = g * Dv[0] + y[q] * il[q];
@@ -1712,7 +1714,7 @@ __device__ __forceinline__ void warp_line_solve(double (&y)[kWK], const double* 
     warp_scan<NV, false>(G, Dv, xin);
     double xp = xin[0], zq = xin[NV - 1];
 #pragma unroll
-    for (int q = kWK - 1; q >= 0; --q) {
+    for (int q = KW - 1; q >= 0; --q) {
         if (q < KE && j0 + q < n) {
             xp = (y[q] - mj[q] * xp) * il[q];
             y[q] = xp;
@@ -1723,11 +1725,11 @@ __device__ __forceinline__ void warp_line_solve(double (&y)[kWK], const double* 
         }
     }
     if (CYC) {
-        // x_0, z_0 live on lane 0; x_{n-1}, z_{n-1} on lane (n-1)/kWK
+        // x_0, z_0 live on lane 0; x_{n-1}, z_{n-1} on lane (n-1)/KW
         const int last = (n - 1) / KE, ql = (n - 1) - last * KE;
         double xl = 0.0, zl = 0.0;
 #pragma unroll
-        for (int q = 0; q < kWK; ++q)
+        for (int q = 0; q < KW; ++q)
             if (q == ql) {
                 xl = y[q];
                 zl = z[CYC ? q : 0];
@@ -1737,41 +1739,62 @@ __device__ __forceinline__ void warp_line_solve(double (&y)[kWK], const double* 
         zl = __shfl_sync(FULL, zl, last);
         const double tau = corner * (x0 + xl) / (1.0 + corner * (z0 + zl));
 #pragma unroll
-        for (int q = 0; q < kWK; ++q) y[q] -= tau * z[CYC ? q : 0];
+        for (int q = 0; q < KW; ++q) y[q] -= tau * z[CYC ? q : 0];
     }
 }
 
 
+// The coarse tail evaluates the assembled rows of launch_rows (Rw = this
+// section's [10][n] block): absent couplings are stored as 0 and their
+// neighbour index is the node itself, so every row is the same 10 products.
 // rhs of circle row (s,t): f - sum of the off-line couplings (smoother.cpp:162-182)
-template <bool ONFLY>
-__device__ __forceinline__ double circle_rhs(const LevelView& L, const double* __restrict__ U,
-                                             const double* __restrict__ F, long off, int b, int s,
-                                             int t) {
-    const int p = s * L.nt + t;
-    const CoefAt<ONFLY> cf{&L, off, b};
+__device__ __forceinline__ double circle_rhs(const LevelView& L, const double* __restrict__ Rw,
+                                             const double* __restrict__ U,
+                                             const double* __restrict__ F, int s, int t) {
+    const int p = s * L.nt + t, n = L.n;
     const Nbr q = neighbours(L, s, t, p);
-    const Row R = make_row_fast(L, cf, s, t, p, q);
     double acc = F[p];
-    if (R.has_sm) acc -= R.sm * U[q.pSM];
-    if (R.has_sp) acc -= R.sp * U[q.pSP];
-    if (R.has_sm) {
-        acc -= R.mm * U[q.pSMTM];
-        acc -= R.mp * U[q.pSMTP];
-    }
-    if (R.has_sp) {
-        acc -= R.pm * U[q.pSPTM];
-        acc -= R.pp * U[q.pSPTP];
-    }
+    acc -= Rw[1 * n + p] * U[q.pSM];
+    acc -= Rw[2 * n + p] * U[q.pSP];
+    acc -= Rw[5 * n + p] * U[q.pSMTM];
+    acc -= Rw[6 * n + p] * U[q.pSMTP];
+    acc -= Rw[7 * n + p] * U[q.pSPTM];
+    acc -= Rw[8 * n + p] * U[q.pSPTP];
     return acc;
 }
 
+// r = f - A u of node p with the assembled row (apply_take order,
+// stencil.cpp:166-171)
+__device__ __forceinline__ double row_residual(const LevelView& L, const double* __restrict__ Rw,
+                                               const double* __restrict__ U,
+                                               const double* __restrict__ F, int p) {
+    int s, t;
+    L.node(p, s, t);
+    const int n = L.n;
+    const Nbr q = neighbours(L, s, t, p);
+    int pph = p;
+    if (s == 0 && L.boundary == 0) pph = t + L.nt / 2 >= L.nt ? t + L.nt / 2 - L.nt : t + L.nt / 2;
+    double acc = 0.0;
+    acc += Rw[p] * U[p];
+    acc += Rw[1 * n + p] * U[q.pSM];
+    acc += Rw[2 * n + p] * U[q.pSP];
+    acc += Rw[3 * n + p] * U[q.pTM];
+    acc += Rw[4 * n + p] * U[q.pTP];
+    acc += Rw[5 * n + p] * U[q.pSMTM];
+    acc += Rw[6 * n + p] * U[q.pSMTP];
+    acc += Rw[7 * n + p] * U[q.pSPTM];
+    acc += Rw[8 * n + p] * U[q.pSPTP];
+    acc += Rw[9 * n + p] * U[pph];
+    return F[p] - acc;
+}
+
 // warp version of origin_solve (2nd-order recurrences as 2x2-map scans)
-template <bool ONFLY>
+template <int KW>
 __device__ void origin_warp(const CoarseLevel& C, double* __restrict__ U,
                             const double* __restrict__ F, long off, int b) {
     const LevelView& L = C.v;
     const int n = L.nt, h = n / 2, nb = n - 2;
-    const int KE = (n + 31) >> 5;  // rows per lane (<= kWK)
+    const int KE = (n + 31) >> 5;  // rows per lane (<= KW)
     const int lane = threadIdx.x & 31, j0 = lane * KE;
     const long o = (long)b * n;
     const double* b1 = C.of.band1 + o;
@@ -1779,13 +1802,14 @@ __device__ void origin_warp(const CoarseLevel& C, double* __restrict__ U,
     const double* r1 = C.of.row1 + o;
     const double* r2 = C.of.row2 + o;
     const double* D = C.of.D + o;
-    double x[kWK];
+    const double* Rw = C.rows + (long)b * 10 * L.n;
+    double x[KW];
     Map2 m = {1.0, 0.0, 0.0, 1.0, 0.0, 0.0};
 #pragma unroll
-    for (int q = 0; q < kWK; ++q) {
+    for (int q = 0; q < KW; ++q) {
         const int i = j0 + q;
         const bool in = q < KE;
-        x[q] = (in && i < n) ? circle_rhs<ONFLY>(L, U, F, off, b, 0, operm(i, h)) : 0.0;
+        x[q] = (in && i < n) ? circle_rhs(L, Rw, U, F, 0, operm(i, h)) : 0.0;
         if (in && i < nb) {
             const double l1 = i >= 1 ? b1[i] : 0.0, l2 = i >= 2 ? b2[i] : 0.0;
             const Map2 mi = {0.0, 1.0, -l2, -l1, 0.0, x[q]};
@@ -1796,7 +1820,7 @@ __device__ void origin_warp(const CoarseLevel& C, double* __restrict__ U,
     warp_scan2(m, true, zm2, zm1);
     double s1 = 0.0, s2 = 0.0;
 #pragma unroll
-    for (int q = 0; q < kWK; ++q) {
+    for (int q = 0; q < KW; ++q) {
         const int i = j0 + q;
         if (q < KE && i < nb) {
             double sum = x[q];
@@ -1816,7 +1840,7 @@ __device__ void origin_warp(const CoarseLevel& C, double* __restrict__ U,
     }
     double xr2 = 0.0, xr1 = 0.0;  // rhs of the closing rows n-2, n-1
 #pragma unroll
-    for (int q = 0; q < kWK; ++q) {
+    for (int q = 0; q < KW; ++q) {
         if (q < KE && j0 + q == n - 2) xr2 = x[q];
         if (q < KE && j0 + q == n - 1) xr1 = x[q];
     }
@@ -1830,7 +1854,7 @@ __device__ void origin_warp(const CoarseLevel& C, double* __restrict__ U,
     if (n - 2 >= C.of.fc2) xn2 -= r2[n - 2] * xn1;
     Map2 g = {1.0, 0.0, 0.0, 1.0, 0.0, 0.0};
 #pragma unroll
-    for (int q = kWK - 1; q >= 0; --q) {
+    for (int q = KW - 1; q >= 0; --q) {
         const int k = j0 + q;
         if (q < KE && k < nb) {
             double gk = x[q] / D[k];
@@ -1846,7 +1870,7 @@ __device__ void origin_warp(const CoarseLevel& C, double* __restrict__ U,
     double xp1, xp2;
     warp_scan2(g, false, xp1, xp2);
 #pragma unroll
-    for (int q = kWK - 1; q >= 0; --q) {
+    for (int q = KW - 1; q >= 0; --q) {
         const int k = j0 + q;
         if (q < KE && k < nb) {
             double xv = x[q];
@@ -1859,7 +1883,7 @@ __device__ void origin_warp(const CoarseLevel& C, double* __restrict__ U,
     }
     __syncwarp();
 #pragma unroll
-    for (int q = 0; q < kWK; ++q) {
+    for (int q = 0; q < KW; ++q) {
         const int k = j0 + q;
         if (q >= KE) continue;
         if (k < nb) U[operm(k, h)] = x[q];
@@ -1868,7 +1892,7 @@ __device__ void origin_warp(const CoarseLevel& C, double* __restrict__ U,
     }
 }
 
-template <bool ONFLY>
+template <int KW>
 __device__ void coarse_smooth(const CoarseLevel& C, int b) {
     const LevelView& L = C.v;
     const long off = (long)b * L.n;
@@ -1876,6 +1900,7 @@ __device__ void coarse_smooth(const CoarseLevel& C, int b) {
     const double* F = C.f + off;
     const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
     const int nt = L.nt;
+    const double* Rw = C.rows + (long)b * 10 * L.n;
     for (int parity = 0; parity < 2; ++parity) {  // circle sweeps (smoother.cpp:95-116)
         const int lines = L.split > parity ? (L.split - parity + 1) / 2 : 0;
         for (int li = warp; li < lines; li += nw) {
@@ -1885,129 +1910,119 @@ __device__ void coarse_smooth(const CoarseLevel& C, int b) {
                 continue;
             }
             if (s == 0 && L.boundary == 0) {
-                origin_warp<ONFLY>(C, U, F, off, b);
+                origin_warp<KW>(C, U, F, off, b);
                 continue;
             }
-            double y[kWK];
+            double y[KW];
             const int KE = (nt + 31) >> 5;
             const int j0 = lane * KE;
 #pragma unroll
-            for (int q = 0; q < kWK; ++q)
-                y[q] = (q < KE && j0 + q < nt) ? circle_rhs<ONFLY>(L, U, F, off, b, s, j0 + q) : 0.0;
+            for (int q = 0; q < KW; ++q)
+                y[q] = (q < KE && j0 + q < nt) ? circle_rhs(L, Rw, U, F, s, j0 + q) : 0.0;
             const long fo = (long)b * L.split * nt + (long)s * nt;
-            warp_line_solve<true>(y, C.cl + fo, C.cm + fo, nt, C.corner[(long)b * L.split + s]);
+            warp_line_solve<true, KW>(y, C.cl + fo, C.cm + fo, nt, C.corner[(long)b * L.split + s]);
             __syncwarp();
 #pragma unroll
-            for (int q = 0; q < kWK; ++q)
+            for (int q = 0; q < KW; ++q)
                 if (q < KE && j0 + q < nt) U[s * nt + j0 + q] = y[q];
         }
         __syncthreads();
     }
     if (L.len <= 0) return;
-    const CoefAt<ONFLY> cf{&L, off, b};
+    const int n = L.n;
     for (int parity = 0; parity < 2; ++parity) {  // radial sweeps (smoother.cpp:118-142)
         const int lines = (nt - parity + 1) / 2;
         for (int li = warp; li < lines; li += nw) {
             const int t = parity + 2 * li;
             const int base = L.split * nt + t * L.len;
-            double y[kWK];
+            double y[KW];
             const int KE = (L.len + 31) >> 5;
             const int j0 = lane * KE;
 #pragma unroll
-            for (int q = 0; q < kWK; ++q) {
+            for (int q = 0; q < KW; ++q) {
                 const int i = j0 + q, s = L.split + i;
                 double acc = 0.0;
                 if (q < KE && i < L.len) {
                     const int p = base + i;
-                    if (L.dir(s)) {
-                        acc = F[p];
-                    } else {
-                        const Nbr nb = neighbours(L, s, t, p);
-                        const Row R = make_row_fast(L, cf, s, t, p, nb);
-                        acc = F[p];
-                        if (s == L.split && R.has_sm) acc -= R.sm * U[nb.pSM];
-                        acc -= R.tm * U[nb.pTM];
-                        acc -= R.tp * U[nb.pTP];
-                        if (R.has_sm) {
-                            acc -= R.mm * U[nb.pSMTM];
-                            acc -= R.mp * U[nb.pSMTP];
-                        }
-                        if (R.has_sp) {
-                            acc -= R.pm * U[nb.pSPTM];
-                            acc -= R.pp * U[nb.pSPTP];
-                        }
-                    }
+                    const Nbr nb = neighbours(L, s, t, p);
+                    acc = F[p];
+                    if (s == L.split) acc -= Rw[1 * n + p] * U[nb.pSM];
+                    acc -= Rw[3 * n + p] * U[nb.pTM];
+                    acc -= Rw[4 * n + p] * U[nb.pTP];
+                    acc -= Rw[5 * n + p] * U[nb.pSMTM];
+                    acc -= Rw[6 * n + p] * U[nb.pSMTP];
+                    acc -= Rw[7 * n + p] * U[nb.pSPTM];
+                    acc -= Rw[8 * n + p] * U[nb.pSPTP];
                 }
                 y[q] = acc;
             }
             const long fo = ((long)b * nt + t) * L.len;
-            warp_line_solve<false>(y, C.rl + fo, C.rm + fo, L.len, 0.0);
+            warp_line_solve<false, KW>(y, C.rl + fo, C.rm + fo, L.len, 0.0);
             __syncwarp();
 #pragma unroll
-            for (int q = 0; q < kWK; ++q)
+            for (int q = 0; q < KW; ++q)
                 if (q < KE && j0 + q < L.len) U[base + j0 + q] = y[q];
         }
         __syncthreads();
     }
 }
 
-template <class T>
-__device__ __forceinline__ T* rebase_ptr(T* p, char* base) {
-    const uintptr_t o = reinterpret_cast<uintptr_t>(p);
-    return o == 0 ? nullptr : reinterpret_cast<T*>(base + (o - 8));
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n\t"
+                 "fence.proxy.async.shared::cta;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// bulk global -> shared copy (TMA engine), completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
 }
 
-__device__ void rebase_level(CoarseLevel& c, char* base) {
-    LevelView& v = c.v;
-    v.r = rebase_ptr(v.r, base);
-    v.h = rebase_ptr(v.h, base);
-    v.k = rebase_ptr(v.k, base);
-    v.sn = rebase_ptr(v.sn, base);
-    v.cs = rebase_ptr(v.cs, base);
-    v.alpha = rebase_ptr(v.alpha, base);
-    v.beta = rebase_ptr(v.beta, base);
-    v.arr = rebase_ptr(v.arr, base);
-    v.art = rebase_ptr(v.art, base);
-    v.att = rebase_ptr(v.att, base);
-    v.det = rebase_ptr(v.det, base);
-    v.rh = rebase_ptr(v.rh, base);
-    v.rk = rebase_ptr(v.rk, base);
-    v.B = 1;
-    c.u = rebase_ptr(c.u, base);
-    c.f = rebase_ptr(c.f, base);
-    c.res = rebase_ptr(c.res, base);
-    c.cl = rebase_ptr(c.cl, base);
-    c.cm = rebase_ptr(c.cm, base);
-    c.corner = rebase_ptr(c.corner, base);
-    c.rl = rebase_ptr(c.rl, base);
-    c.rm = rebase_ptr(c.rm, base);
-    c.of.band1 = rebase_ptr(c.of.band1, base);
-    c.of.band2 = rebase_ptr(c.of.band2, base);
-    c.of.row1 = rebase_ptr(c.of.row1, base);
-    c.of.row2 = rebase_ptr(c.of.row2, base);
-    c.of.D = rebase_ptr(c.of.D, base);
-    c.w.rwb = rebase_ptr(c.w.rwb, base);
-    c.w.rwa = rebase_ptr(c.w.rwa, base);
-    c.w.awb = rebase_ptr(c.w.awb, base);
-    c.w.awa = rebase_ptr(c.w.awa, base);
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
 }
 
 // Executes the op program; `bb` is the section index used for per-section
 // arrays (0 when the data is shared-memory resident and section-sliced).
-template <bool ONFLY>
+template <int KW>
 __device__ __forceinline__ void run_prog(const CoarseLevel* lv, const EnvFactor& env,
-                                         const int* __restrict__ prog, int nops, int bb) {
+                                         const int* __restrict__ prog, int nops, int bb,
+                                         unsigned long long* trace = nullptr) {
     for (int i = 0; i < nops; ++i) {
         const int op = prog[i] & 255, l = prog[i] >> 8;
         const CoarseLevel& C = lv[l];
         const long off = (long)bb * C.v.n;
         switch (op) {
             case OP_SMOOTH:
-                coarse_smooth<ONFLY>(C, bb);
+                coarse_smooth<KW>(C, bb);
                 break;
             case OP_RESIDUAL:
                 for (int p = threadIdx.x; p < C.v.n; p += blockDim.x)
-                    C.res[off + p] = apply_node<ONFLY, 1>(C.v, C.u + off, C.f + off, off, bb, p);
+                    C.res[off + p] =
+                        row_residual(C.v, C.rows + (long)bb * 10 * C.v.n, C.u + off, C.f + off, p);
                 break;
             case OP_RESTRICT: {
                 const CoarseLevel& D = lv[l + 1];
@@ -2024,7 +2039,20 @@ __device__ __forceinline__ void run_prog(const CoarseLevel* lv, const EnvFactor&
                 break;
             }
             default: {  // OP_COARSE: u = f, envelope LDL^T (multigrid.cpp:183-187)
-                if (threadIdx.x == 0) {
+                if (env.inv) {  // dense inverse: one row per thread
+                    const int n = env.n;
+                    const double* A = env.inv + (long)bb * n * n;
+                    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+                        double a0 = 0.0, a1 = 0.0;
+                        int j = 0;
+                        for (; j + 1 < n; j += 2) {
+                            a0 += A[(long)j * n + i] * C.f[off + j];
+                            a1 += A[(long)(j + 1) * n + i] * C.f[off + j + 1];
+                        }
+                        if (j < n) a0 += A[(long)j * n + i] * C.f[off + j];
+                        C.u[off + i] = a0 + a1;
+                    }
+                } else if (threadIdx.x == 0) {
                     double* x = C.u + off;
                     for (int k = 0; k < env.n; ++k) x[k] = C.f[off + k];
                     env_solve(env, bb, x);
@@ -2033,57 +2061,65 @@ __device__ __forceinline__ void run_prog(const CoarseLevel* lv, const EnvFactor&
             }
         }
         __syncthreads();
+        if (trace && threadIdx.x == 0) trace[2 + i] = globaltimer();
     }
 }
 
-template <bool ONFLY>
+template <int KW>
 __global__ void __launch_bounds__(512) k_coarse_cycle(const __grid_constant__ CoarseParams cp,
                                                       const int* __restrict__ prog, int nops,
                                                       const int* __restrict__ active) {
     extern __shared__ __align__(16) char sbuf[];
-    __shared__ CoarseLevel slv[kMaxCoarse];
-    __shared__ EnvFactor senv;
+    __shared__ __align__(16) TailImage simg;
     const int b = blockIdx.x;
     if (active && !active[b]) return;
-    if (!cp.resident) {
-        run_prog<ONFLY>(cp.lv - cp.first, cp.env, prog, nops, b);
-        return;
-    }
-    // stage this section's slice of every tail array into shared memory: warps
-    // take descriptors round-robin and issue asynchronous copies, one wait
-    {
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-        for (int c = warp; c < cp.ncopy; c += nw) {
-            const CopyDesc d = cp.copies[c];
-            const char* src = static_cast<const char*>(d.src) + (long)b * d.stride;
-            const int words = d.bytes >> 3;
-            for (int w = lane; w < words; w += 32)
-                __pipeline_memcpy_async(sbuf + d.dst + 8 * w, src + 8 * w, 8);
-            if ((d.bytes & 7) && lane == 0)  // int arrays of odd length
-                __pipeline_memcpy_async(sbuf + d.dst + (d.bytes - 4), src + (d.bytes - 4), 4);
-        }
-        __pipeline_commit();
-        __pipeline_wait_prior(0);
-    }
-    const int nl = cp.lv[0].v.nr == 0 ? 0 : kMaxCoarse;
-    if (threadIdx.x < kMaxCoarse) {
-        CoarseLevel c = cp.lv[threadIdx.x];
-        if (c.v.nr > 0) rebase_level(c, sbuf);
-        slv[threadIdx.x] = c;
-    }
+    unsigned long long* trace = b == 0 ? cp.trace : nullptr;
+    if (trace && threadIdx.x == 0) trace[0] = globaltimer();
+    // stage this section's slice of every tail array into shared memory: one
+    // thread per array issues a bulk (TMA) copy of its 16-byte aligned part,
+    // completing on an mbarrier; leftovers go through cp.async
+    __shared__ __align__(8) unsigned long long sbar;
+    __shared__ unsigned stx;
     if (threadIdx.x == 0) {
-        EnvFactor e = cp.env;
-        e.fc = rebase_ptr(e.fc, sbuf);
-        e.ro = rebase_ptr(e.ro, sbuf);
-        e.L = rebase_ptr(e.L, sbuf);
-        e.D = rebase_ptr(e.D, sbuf);
-        senv = e;
+        mbar_init(&sbar, 1);
+        stx = 0;
     }
-    (void)nl;
     __syncthreads();
-    run_prog<ONFLY>(slv - cp.first, senv, prog, nops, 0);
+    for (int c = threadIdx.x; c < cp.ncopy; c += blockDim.x) {
+        const CopyDesc d = cp.copies[c];
+        const char* src = static_cast<const char*>(d.src) + (long)b * d.stride;
+        const int bulk = (reinterpret_cast<uintptr_t>(src) & 15) == 0 ? (d.bytes & ~15) : 0;
+        if (bulk > 0) {
+            bulk_g2s(sbuf + d.dst, src, bulk, &sbar);
+            atomicAdd(&stx, (unsigned)bulk);
+        }
+        for (int o = bulk; o + 8 <= d.bytes; o += 8)
+            __pipeline_memcpy_async(sbuf + d.dst + o, src + o, 8);
+        if (d.bytes & 7)  // int arrays of odd length
+            __pipeline_memcpy_async(sbuf + d.dst + (d.bytes - 4), src + (d.bytes - 4), 4);
+    }
+    __pipeline_commit();
+    {  // level table image, rebased onto this block's shared window
+        const unsigned long long base = reinterpret_cast<uintptr_t>(sbuf);
+        unsigned long long* w = reinterpret_cast<unsigned long long*>(&simg);
+        constexpr int words = sizeof(TailImage) / 8;
+        for (int i = threadIdx.x; i < words; i += blockDim.x) {
+            unsigned long long x = cp.image[i];
+            if (((cp.image_mask[i >> 5] >> (i & 31)) & 1u) && x) x = x - 8 + base;
+            w[i] = x;
+        }
+    }
+    __syncthreads();
+    if (trace && threadIdx.x == 0) trace[nops + 2] = globaltimer();
+    if (threadIdx.x == 0) mbar_arrive_tx(&sbar, stx);
+    __pipeline_wait_prior(0);
+    mbar_wait(&sbar, 0);
+    if (trace && threadIdx.x == 0) trace[nops + 3] = globaltimer();
+    __syncthreads();
+    if (trace && threadIdx.x == 0) trace[1] = globaltimer();
+    run_prog<KW>(simg.lv - cp.first, simg.env, prog, nops, 0, trace);
     // the top level's correction goes back to global memory
-    const CoarseLevel& top = slv[0];
+    const CoarseLevel& top = simg.lv[0];
     for (int p = threadIdx.x; p < top.v.n; p += blockDim.x)
         cp.top_u_global[(long)b * top.v.n + p] = top.u[p];
 }
@@ -2523,13 +2559,25 @@ void launch_flush(double* buf, long n, cudaStream_t st) {
 namespace pmg {
 void launch_coarse_cycle(const CoarseParams& cp, const int* prog, int nops, int B, bool onfly,
                          const int* active, cudaStream_t st) {
-    const size_t sm = cp.resident ? (size_t)cp.smem_bytes : 0;
-    if (onfly) {
-        set_smem(k_coarse_cycle<true>, sm);
-        k_coarse_cycle<true><<<B, 512, sm, st>>>(cp, prog, nops, active);
-    } else {
-        set_smem(k_coarse_cycle<false>, sm);
-        k_coarse_cycle<false><<<B, 512, sm, st>>>(cp, prog, nops, active);
+    (void)onfly;  // the tail evaluates assembled rows in both stencil modes
+    const size_t sm = (size_t)cp.smem_bytes;
+    switch (cp.kw) {
+        case 1:
+            set_smem(k_coarse_cycle<1>, sm);
+            k_coarse_cycle<1><<<B, 512, sm, st>>>(cp, prog, nops, active);
+            break;
+        case 2:
+            set_smem(k_coarse_cycle<2>, sm);
+            k_coarse_cycle<2><<<B, 512, sm, st>>>(cp, prog, nops, active);
+            break;
+        case 4:
+            set_smem(k_coarse_cycle<4>, sm);
+            k_coarse_cycle<4><<<B, 512, sm, st>>>(cp, prog, nops, active);
+            break;
+        default:
+            set_smem(k_coarse_cycle<8>, sm);
+            k_coarse_cycle<8><<<B, 512, sm, st>>>(cp, prog, nops, active);
+            break;
     }
 }
 }  // namespace pmg

@@ -25,6 +25,7 @@ struct EnvFactor {
     const long* ro;     // [n+1] row offsets into L
     const double* L;    // [B][nnz]
     const double* D;    // [B][n]
+    const double* inv;  // [B][n][n] A^-1 column-major (coarse tail, n <= 64) or null
     long nnz;
     int n;
 };
@@ -42,6 +43,7 @@ struct CoarseLevel {
     double *u, *f, *res;
     const double *cl, *cm, *corner;  // circle factors [B][split*nt], corner [B][split]
     const double *rl, *rm;           // radial factors [B][nt*len]
+    const double* rows;              // assembled rows [B][10][n] (launch_rows)
     OriginFactor of;
     Weights w;  // this level as the fine level of a transfer
 };
@@ -58,6 +60,15 @@ struct CopyDesc {
     int bytes;        // bytes to copy
     int dst;          // byte offset in dynamic shared memory
 };
+// Shared-memory image of the tail's level table: the host writes it with
+// shared-memory offsets (+8, 0 = null) in every pointer field and a bit mask of
+// the pointer words; the block copies it in and rebases the marked words.
+struct TailImage {
+    CoarseLevel lv[kMaxCoarse];
+    EnvFactor env;
+};
+static_assert(sizeof(TailImage) % 8 == 0, "TailImage is copied as 8-byte words");
+
 struct CoarseParams {
     CoarseLevel lv[kMaxCoarse];
     EnvFactor env;
@@ -66,10 +77,16 @@ struct CoarseParams {
     // 0 = null; the block copies `ncopy` arrays in, runs, and writes the top
     // level's u back to `top_u_global`
     int resident;
+    int kw;  // rows per lane of the warp line solves (1, 2, 4, 8)
     int ncopy;
     int smem_bytes;
     const CopyDesc* copies;
+    const unsigned long long* image;  // TailImage words
+    const unsigned* image_mask;       // bit i: word i is a pointer
     double* top_u_global;
+    // diagnostics (PMG_TAIL_TRACE): %globaltimer of block 0 at entry, after
+    // staging and after every op; null = off
+    unsigned long long* trace;
 };
 
 // Runs an op program (op | level << 8) over the coarse levels, one block per
@@ -161,6 +178,8 @@ void launch_circle_z(const LevelView& L, const double* cil, const double* cm, do
                      cudaStream_t st);
 void launch_factor_radial(const LevelView& L, bool onfly, double* ril, double* rm, int* bad,
                           cudaStream_t st);
+// assembled rows [B][10][n] of a coarse-tail level (see k_rows)
+void launch_rows(const LevelView& L, bool onfly, double* rows, cudaStream_t st);
 // f = A u on the finest level for seeded RHS (same as launch_apply mode 0)
 
 }  // namespace pmg

@@ -160,6 +160,35 @@ __global__ void k_circle_z(LevelView L, const double* cl, const double* cm, doub
     }
 }
 
+// Assembled stencil rows of a coarse-tail level: rows[b][k][p], k = d, sm,
+// sp, tm, tp, mm, mp, pm, pp, ph (make_row, stencil.cpp:44-137), couplings
+// the row does not have stored as 0 so the tail evaluates every row with the
+// same 10 multiply-adds.
+template <bool ONFLY>
+__global__ void k_rows(LevelView L, double* __restrict__ rows) {
+    const int b = blockIdx.y;
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= L.n) return;
+    int s, t;
+    L.node(p, s, t);
+    const long off = (long)b * L.n;
+    const CoefAt<ONFLY> cf{&L, off, b};
+    const Nbr q = neighbours(L, s, t, p);
+    const Row R = make_row_fast(L, cf, s, t, p, q);
+    double* o = rows + (long)b * 10 * L.n + p;
+    const long n = L.n;
+    o[0] = R.d;
+    o[1 * n] = R.has_sm ? R.sm : 0.0;
+    o[2 * n] = R.has_sp ? R.sp : 0.0;
+    o[3 * n] = R.ident ? 0.0 : R.tm;
+    o[4 * n] = R.ident ? 0.0 : R.tp;
+    o[5 * n] = R.has_sm ? R.mm : 0.0;
+    o[6 * n] = R.has_sm ? R.mp : 0.0;
+    o[7 * n] = R.has_sp ? R.pm : 0.0;
+    o[8 * n] = R.has_sp ? R.pp : 0.0;
+    o[9 * n] = R.origin ? R.ph : 0.0;
+}
+
 }  // namespace
 
 void launch_circle_z(const LevelView& L, const double* cil, const double* cm, double* cz,
@@ -181,6 +210,14 @@ void launch_factor_circle(const LevelView& L, bool onfly, double* cil, double* c
         k_factor_circle<true><<<grid, 64, 0, st>>>(L, cil, cm, corner, bad);
     else
         k_factor_circle<false><<<grid, 64, 0, st>>>(L, cil, cm, corner, bad);
+}
+
+void launch_rows(const LevelView& L, bool onfly, double* rows, cudaStream_t st) {
+    dim3 grid((L.n + 127) / 128, L.B);
+    if (onfly)
+        k_rows<true><<<grid, 128, 0, st>>>(L, rows);
+    else
+        k_rows<false><<<grid, 128, 0, st>>>(L, rows);
 }
 
 void launch_factor_radial(const LevelView& L, bool onfly, double* ril, double* rm, int* bad,

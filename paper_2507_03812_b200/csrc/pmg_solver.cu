@@ -177,6 +177,7 @@ struct Level {
     double *arr = nullptr, *art = nullptr, *att = nullptr, *det = nullptr;
     double *cil = nullptr, *cm = nullptr, *corner = nullptr, *ril = nullptr, *rm = nullptr;
     double* cz = nullptr;  // Sherman-Morrison vectors of the circle lines (exact path)
+    double* rows = nullptr;  // assembled rows [B][10][n] (coarse-tail levels)
     double *ob1 = nullptr, *ob2 = nullptr, *or1 = nullptr, *or2 = nullptr, *oD = nullptr;
     int ofc1 = 0, ofc2 = 0;
     Weights w{};
@@ -209,6 +210,7 @@ struct Solver {
     CoarseParams coarse_params{};
     int* d_prog[3] = {nullptr, nullptr, nullptr};
     int prog_len[3] = {0, 0, 0};
+    std::vector<int> h_prog[3];
     // CUDA graph of one cycle + residual norm + convergence check
     cudaGraphExec_t cycle_exec = nullptr;
     long long cycle_nodes = 0;
@@ -503,14 +505,12 @@ struct Solver {
             const HostGrid& g = lv[l].g;
             const long n = g.n(), nr = g.nr(), nt = g.nt(), sp = g.split, len = nr - sp;
             const bool coarsest = l == L - 1;
-            long d = 2 * nr + 6 * nt + 2 * nr;     // r, h, rh, k, sn, cs, rk(+pad), alpha, beta
-            if (!onfly) d += 4 * n;                 // arr art att det
-            d += 2 * n;                             // u, f
+            long d = 2 * n;                         // u, f
             if (!coarsest) {
-                d += n;                             // res
+                d += 11 * n;                        // res, assembled rows
                 d += 2 * sp * nt + sp + 2 * nt * len + 5 * nt + 2 * nr + 2 * nt;
             } else {
-                d += lv[l].env.nnz + n + n / 2 + n + 2;  // L, D, fc (ints), ro (longs)
+                d += n <= 64 ? n * n : lv[l].env.nnz + n + n / 2 + n + 2;  // inv | L, D, fc, ro
             }
             (void)top;
             return d * 8 + 40 * 16;                 // + alignment slack
@@ -549,20 +549,13 @@ struct Solver {
             CoarseLevel& c = coarse_params.lv[l - start];
             c.v = V.v;
             LevelView& v = c.v;
-            v.r = static_cast<double*>(place(V.v.r, 0, nr, 8));
-            v.h = static_cast<double*>(place(V.v.h, 0, nr - 1, 8));
-            v.rh = static_cast<double*>(place(V.v.rh, 0, nr - 1, 8));
-            v.k = static_cast<double*>(place(V.v.k, 0, nt, 8));
-            v.rk = static_cast<double*>(place(V.v.rk, 0, nt, 8));
-            v.sn = static_cast<double*>(place(V.v.sn, 0, nt, 8));
-            v.cs = static_cast<double*>(place(V.v.cs, 0, nt, 8));
-            v.alpha = static_cast<double*>(place(V.v.alpha, nr * 8, nr, 8));
-            v.beta = static_cast<double*>(place(V.v.beta, nr * 8, nr, 8));
-            if (!onfly) {
-                v.arr = static_cast<double*>(place(V.v.arr, n * 8, n, 8));
-                v.art = static_cast<double*>(place(V.v.art, n * 8, n, 8));
-                v.att = static_cast<double*>(place(V.v.att, n * 8, n, 8));
-                v.det = static_cast<double*>(place(V.v.det, n * 8, n, 8));
+            // the tail works from assembled rows: geometry/coefficients stay behind
+            v.r = v.h = v.rh = v.k = v.rk = v.sn = v.cs = v.alpha = v.beta = nullptr;
+            v.arr = v.art = v.att = v.det = nullptr;
+            if (!coarsest) {
+                V.rows = alloc<double>((size_t)B * 10 * n, false);
+                launch_rows(V.v, onfly, V.rows, stream);
+                c.rows = static_cast<double*>(place(V.rows, 10 * n * 8, 10 * n, 8));
             }
             c.u = static_cast<double*>(place(top ? V.u : nullptr, n * 8, n, 8));
             c.f = static_cast<double*>(place(top ? V.f : nullptr, n * 8, n, 8));
@@ -591,10 +584,18 @@ struct Solver {
             } else {
                 const EnvFactor& E = V.env;
                 coarse_params.env = E;
-                coarse_params.env.fc = static_cast<int*>(place(E.fc, 0, E.n, 4));
-                coarse_params.env.ro = static_cast<long*>(place(E.ro, 0, E.n + 1, 8));
-                coarse_params.env.L = static_cast<double*>(place(E.L, E.nnz * 8, E.nnz, 8));
-                coarse_params.env.D = static_cast<double*>(place(E.D, E.n * 8, E.n, 8));
+                coarse_params.env.fc = nullptr;
+                coarse_params.env.ro = nullptr;
+                coarse_params.env.L = coarse_params.env.D = coarse_params.env.inv = nullptr;
+                if (E.inv) {
+                    coarse_params.env.inv =
+                        static_cast<double*>(place(E.inv, (long)E.n * E.n * 8, (long)E.n * E.n, 8));
+                } else {
+                    coarse_params.env.fc = static_cast<int*>(place(E.fc, 0, E.n, 4));
+                    coarse_params.env.ro = static_cast<long*>(place(E.ro, 0, E.n + 1, 8));
+                    coarse_params.env.L = static_cast<double*>(place(E.L, E.nnz * 8, E.nnz, 8));
+                    coarse_params.env.D = static_cast<double*>(place(E.D, E.n * 8, E.n, 8));
+                }
             }
         }
         if (off > 220 * 1024) {  // budget estimate too small: stay non-resident
@@ -602,16 +603,78 @@ struct Solver {
             return;
         }
         coarse_params.resident = 1;
+        {  // level table image + pointer-word mask (see TailImage)
+            TailImage img;
+            std::memset(&img, 0, sizeof img);
+            for (int i = 0; i < kMaxCoarse; ++i) {
+                img.lv[i] = coarse_params.lv[i];
+                if (img.lv[i].v.nr > 0) img.lv[i].v.B = 1;
+            }
+            img.env = coarse_params.env;
+            constexpr size_t words = sizeof(TailImage) / 8;
+            std::vector<unsigned> mask((words + 31) / 32, 0u);
+            auto mark = [&](size_t byte) {
+                const size_t w = byte / 8;
+                mask[w >> 5] |= 1u << (w & 31);
+            };
+            for (int i = 0; i < kMaxCoarse; ++i) {
+                const size_t c = offsetof(TailImage, lv) + i * sizeof(CoarseLevel);
+                const size_t v = c + offsetof(CoarseLevel, v);
+                for (size_t f : {offsetof(LevelView, r), offsetof(LevelView, h),
+                                 offsetof(LevelView, k), offsetof(LevelView, sn),
+                                 offsetof(LevelView, cs), offsetof(LevelView, alpha),
+                                 offsetof(LevelView, beta), offsetof(LevelView, arr),
+                                 offsetof(LevelView, art), offsetof(LevelView, att),
+                                 offsetof(LevelView, det), offsetof(LevelView, rh),
+                                 offsetof(LevelView, rk)})
+                    mark(v + f);
+                for (size_t f : {offsetof(CoarseLevel, u), offsetof(CoarseLevel, f),
+                                 offsetof(CoarseLevel, res), offsetof(CoarseLevel, cl),
+                                 offsetof(CoarseLevel, cm), offsetof(CoarseLevel, corner),
+                                 offsetof(CoarseLevel, rl), offsetof(CoarseLevel, rm),
+                                 offsetof(CoarseLevel, rows)})
+                    mark(c + f);
+                const size_t o = c + offsetof(CoarseLevel, of);
+                for (size_t f : {offsetof(OriginFactor, band1), offsetof(OriginFactor, band2),
+                                 offsetof(OriginFactor, row1), offsetof(OriginFactor, row2),
+                                 offsetof(OriginFactor, D)})
+                    mark(o + f);
+                const size_t w = c + offsetof(CoarseLevel, w);
+                for (size_t f : {offsetof(Weights, rwb), offsetof(Weights, rwa),
+                                 offsetof(Weights, awb), offsetof(Weights, awa)})
+                    mark(w + f);
+            }
+            const size_t e = offsetof(TailImage, env);
+            for (size_t f : {offsetof(EnvFactor, fc), offsetof(EnvFactor, ro), offsetof(EnvFactor, L),
+                             offsetof(EnvFactor, D), offsetof(EnvFactor, inv)})
+                mark(e + f);
+            std::vector<unsigned long long> iw(words);
+            std::memcpy(iw.data(), &img, sizeof img);
+            coarse_params.image = upload(iw);
+            coarse_params.image_mask = upload(mask);
+        }
+        int kw = 1;
+        for (int l = start; l < L - 1; ++l) {
+            const HostGrid& g = lv[l].g;
+            const int m = std::max(g.nt(), g.nr() - g.split);
+            while (32 * kw < m) kw *= 2;
+        }
+        coarse_params.kw = kw;
         coarse_params.ncopy = static_cast<int>(plan.size());
         coarse_params.smem_bytes = static_cast<int>((off + 15) & ~15L);
         coarse_params.copies = upload(plan);
         coarse_params.top_u_global = lv[start].u;
+        int maxlen = 0;
         for (int type = 0; type < 3; ++type) {
             std::vector<int> prog;
             gen_prog(start, type, prog);
             d_prog[type] = upload(prog);
             prog_len[type] = static_cast<int>(prog.size());
+            h_prog[type] = prog;
+            maxlen = std::max(maxlen, prog_len[type]);
         }
+        if (std::getenv("PMG_TAIL_TRACE"))
+            coarse_params.trace = alloc<unsigned long long>(maxlen + 4);
     }
 
     void release(double* p) {
@@ -694,7 +757,7 @@ struct Solver {
         const LevelView HL = host_view(V);
         std::vector<int> nodes(n);
         for (int i = 0; i < n; ++i) nodes[i] = i;
-        std::vector<double> Lall, Dall;
+        std::vector<double> Lall, Dall, inv;
         std::vector<int> fc;
         std::vector<long> ro;
         for (int b = 0; b < B; ++b) {
@@ -710,6 +773,20 @@ struct Solver {
             }
             std::copy(E.L.begin(), E.L.end(), Lall.begin() + (size_t)b * E.L.size());
             std::copy(E.D.begin(), E.D.end(), Dall.begin() + (size_t)b * n);
+            if (n <= 64) {  // dense inverse for the one-block coarse tail
+                if (b == 0) inv.resize((size_t)B * n * n);
+                std::vector<double> x(n);
+                for (int j = 0; j < n; ++j) {
+                    std::fill(x.begin(), x.end(), 0.0);
+                    x[j] = 1.0;
+                    for (int i = 0; i < n; ++i)
+                        for (int k = E.fc[i]; k < i; ++k) x[i] -= E.at(i, k) * x[k];
+                    for (int i = 0; i < n; ++i) x[i] /= E.D[i];
+                    for (int i = n - 1; i >= 0; --i)
+                        for (int k = E.fc[i]; k < i; ++k) x[k] -= E.at(i, k) * x[i];
+                    std::copy(x.begin(), x.end(), inv.begin() + ((size_t)b * n + j) * n);
+                }
+            }
         }
         V.env.n = n;
         V.env.nnz = ro.back();
@@ -717,6 +794,7 @@ struct Solver {
         V.env.ro = upload(ro);
         V.env.L = upload(Lall);
         V.env.D = upload(Dall);
+        V.env.inv = inv.empty() ? nullptr : upload(inv);
     }
 
     // interpolation weights of this level as the fine grid (interpolation.cpp:19-36)
@@ -835,6 +913,27 @@ struct Solver {
         launches = l0;
     }
 
+    // PMG_TAIL_TRACE: per-op durations of the last coarse-tail launch (stderr)
+    void print_tail_trace() {
+        const std::vector<int>& prog = h_prog[set.cycle];
+        std::vector<unsigned long long> t(prog.size() + 4);
+        PMG_CUDA(cudaMemcpy(t.data(), coarse_params.trace, t.size() * 8, cudaMemcpyDeviceToHost));
+        static const char* names[] = {"smooth", "residual", "restrict", "prolong", "coarse"};
+        const size_t np = prog.size();
+        std::fprintf(stderr, "tail trace: staging %.2f us (issue %.2f, wait %.2f, rebase %.2f)\n",
+                     (t[1] - t[0]) * 1e-3, (t[np + 2] - t[0]) * 1e-3,
+                     (t[np + 3] - t[np + 2]) * 1e-3, (t[1] - t[np + 3]) * 1e-3);
+        double sum[5][kMaxCoarse] = {};
+        for (size_t i = 0; i < prog.size(); ++i)
+            sum[prog[i] & 255][(prog[i] >> 8) - coarse_start] += (t[2 + i] - t[1 + i]) * 1e-3;
+        for (int o = 0; o < 5; ++o)
+            for (int l = 0; l < kMaxCoarse; ++l)
+                if (sum[o][l] > 0)
+                    std::fprintf(stderr, "tail trace: level %d %-8s %.2f us\n", coarse_start + l,
+                                 names[o], sum[o][l]);
+        std::fprintf(stderr, "tail trace: total %.2f us\n", (t[prog.size() + 1] - t[0]) * 1e-3);
+    }
+
     int solve(pmg_report* reports, double* history, int history_cap) {
         PMG_CUDA(cudaSetDevice(device));
         cudaEvent_t e0, e1;
@@ -878,6 +977,7 @@ struct Solver {
         PMG_CUDA(cudaGetLastError());
         last_solve_ms = ms;
         collect_profile();
+        if (coarse_params.trace) print_tail_trace();
         // reports
         std::vector<int> h_it(B), h_conv(B);
         std::vector<double> h_hist((size_t)B * hist_cap);
