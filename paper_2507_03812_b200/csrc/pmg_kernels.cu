@@ -25,6 +25,15 @@ namespace pmg {
 
 namespace cg = cooperative_groups;
 
+// Programmatic dependent launch: every kernel of the solve lets the next one
+// in the stream start launching at once and waits for its predecessor's
+// results before touching them (griddepcontrol; no-ops without the launch
+// attribute).
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -681,6 +690,7 @@ __global__ void __launch_bounds__(256) k_apply(LevelView L, const double* __rest
                                                double* __restrict__ out,
                                                double* __restrict__ partials, int norm_type,
                                                const int* __restrict__ active) {
+    pdl_enter();
     constexpr int NPT = 2;
     const int b = blockIdx.y;
     if (active && !active[b]) return;
@@ -752,6 +762,7 @@ __global__ void __launch_bounds__(256, 4) k_apply_tiled(LevelView L, TileGeom G,
                                                         double* __restrict__ partials,
                                                         int norm_type,
                                                         const int* __restrict__ active) {
+    pdl_enter();
     __shared__ double sU[kTH], sArr[kTH], sArt[kTH], sAtt[kTH], sDet[kTH], sF[kTS * kTR];
     __shared__ double red[8];
     const int b = blockIdx.y;
@@ -940,6 +951,7 @@ __global__ void __launch_bounds__(512) k_circle(LevelView L, double* __restrict_
                                                 OriginFactor of, int parity, int serial,
                                                 int exact_rings,
                                                 const int* __restrict__ active) {
+    pdl_enter();
     extern __shared__ double smem[];
     const int b = blockIdx.y;
     if (active && !active[b]) return;
@@ -1009,6 +1021,7 @@ __global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict_
                                                 const double* __restrict__ ril,
                                                 const double* __restrict__ rm, int parity,
                                                 int serial, const int* __restrict__ active) {
+    pdl_enter();
     extern __shared__ double smem[];
     const int b = blockIdx.y;
     if (active && !active[b]) return;
@@ -1347,6 +1360,7 @@ __global__ void __launch_bounds__(256) k_radial_cl(LevelView L, double* __restri
                                                    const double* __restrict__ ril,
                                                    const double* __restrict__ rm, int parity,
                                                    const int* __restrict__ active) {
+    pdl_enter();
     extern __shared__ double smem[];
     __shared__ double xch[8];
     cg::cluster_group cl = cg::this_cluster();
@@ -1435,6 +1449,7 @@ __global__ void __launch_bounds__(256) k_circle_cl(LevelView L, double* __restri
                                                    const double* __restrict__ cm,
                                                    const double* __restrict__ corner, int s_first,
                                                    const int* __restrict__ active) {
+    pdl_enter();
     extern __shared__ double smem[];
     __shared__ double xch[8];
     cg::cluster_group cl = cg::this_cluster();
@@ -1488,6 +1503,15 @@ __global__ void __launch_bounds__(256) k_circle_cl(LevelView L, double* __restri
 // ---------------------------------------------------------------- transfers
 // restrict_transpose (interpolation.cpp:97-143) fused with
 // mask_dirichlet_rows (multigrid.cpp:146-153) and the coarse u = 0 (:204).
+// Loads of vectors another CTA of the same kernel may have written (the
+// cluster-wide multigrid kernel) bypass L1: ld.global.cg.
+template <bool CG>
+__device__ __forceinline__ double ldv(const double* p) {
+    if (CG) return __ldcg(p);
+    return *p;
+}
+
+template <bool CG = false>
 __device__ __forceinline__ void restrict_node(const LevelView& F, const LevelView& C,
                                               const Weights& w, const double* __restrict__ R,
                                               double* __restrict__ cf, double* __restrict__ cu,
@@ -1497,18 +1521,18 @@ __device__ __forceinline__ void restrict_node(const LevelView& F, const LevelVie
     const int sf = 2 * sc, tf = 2 * tc;
     const int tdn = tf == 0 ? F.nt - 1 : tf - 1;
     const int tup = tf + 1;
-    double acc = R[F.idx(sf, tf)];
-    if (sf > 0) acc += w.rwa[sf - 1] * R[F.idx(sf - 1, tf)];
-    if (sf < F.nr - 1) acc += w.rwb[sf + 1] * R[F.idx(sf + 1, tf)];
-    acc += w.awa[tdn] * R[F.idx(sf, tdn)];
-    acc += w.awb[tup] * R[F.idx(sf, tup)];
+    double acc = ldv<CG>(R + F.idx(sf, tf));
+    if (sf > 0) acc += w.rwa[sf - 1] * ldv<CG>(R + F.idx(sf - 1, tf));
+    if (sf < F.nr - 1) acc += w.rwb[sf + 1] * ldv<CG>(R + F.idx(sf + 1, tf));
+    acc += w.awa[tdn] * ldv<CG>(R + F.idx(sf, tdn));
+    acc += w.awb[tup] * ldv<CG>(R + F.idx(sf, tup));
     if (sf > 0) {
-        acc += w.rwa[sf - 1] * w.awa[tdn] * R[F.idx(sf - 1, tdn)];
-        acc += w.rwa[sf - 1] * w.awb[tup] * R[F.idx(sf - 1, tup)];
+        acc += w.rwa[sf - 1] * w.awa[tdn] * ldv<CG>(R + F.idx(sf - 1, tdn));
+        acc += w.rwa[sf - 1] * w.awb[tup] * ldv<CG>(R + F.idx(sf - 1, tup));
     }
     if (sf < F.nr - 1) {
-        acc += w.rwb[sf + 1] * w.awa[tdn] * R[F.idx(sf + 1, tdn)];
-        acc += w.rwb[sf + 1] * w.awb[tup] * R[F.idx(sf + 1, tup)];
+        acc += w.rwb[sf + 1] * w.awa[tdn] * ldv<CG>(R + F.idx(sf + 1, tdn));
+        acc += w.rwb[sf + 1] * w.awb[tup] * ldv<CG>(R + F.idx(sf + 1, tup));
     }
     if (mask && C.dir(sc)) acc = 0.0;
     cf[pc] = acc;
@@ -1522,6 +1546,7 @@ __global__ void __launch_bounds__(256) k_restrict(LevelView F, LevelView C, Weig
                                                   double* __restrict__ cf,
                                                   double* __restrict__ cu, int mask,
                                                   const int* __restrict__ active) {
+    pdl_enter();
     const int b = blockIdx.y;
     if (active && !active[b]) return;
     const int pc = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1530,7 +1555,7 @@ __global__ void __launch_bounds__(256) k_restrict(LevelView F, LevelView C, Weig
                   cu ? cu + (long)b * C.n : nullptr, mask, pc);
 }
 
-template <bool ADD>
+template <bool ADD, bool CG = false>
 __device__ __forceinline__ void prolong_node(const LevelView& F, const LevelView& C,
                                              const Weights& w, const double* __restrict__ X,
                                              double* __restrict__ Y, int p) {
@@ -1541,18 +1566,18 @@ __device__ __forceinline__ void prolong_node(const LevelView& F, const LevelView
     const int tcu = tc + 1 == C.nt ? 0 : tc + 1;
     double v;
     if (!ro && !so) {
-        v = X[C.idx(sc, tc)];
+        v = ldv<CG>(X + C.idx(sc, tc));
     } else if (ro && !so) {
-        v = w.rwb[sf] * X[C.idx(sc, tc)] + w.rwa[sf] * X[C.idx(sc + 1, tc)];
+        v = w.rwb[sf] * ldv<CG>(X + C.idx(sc, tc)) + w.rwa[sf] * ldv<CG>(X + C.idx(sc + 1, tc));
     } else if (!ro && so) {
-        v = w.awb[tf] * X[C.idx(sc, tc)] + w.awa[tf] * X[C.idx(sc, tcu)];
+        v = w.awb[tf] * ldv<CG>(X + C.idx(sc, tc)) + w.awa[tf] * ldv<CG>(X + C.idx(sc, tcu));
     } else {
         const double wb = w.rwb[sf], wa = w.rwa[sf], vb = w.awb[tf], va = w.awa[tf];
-        v = wb * vb * X[C.idx(sc, tc)] + wb * va * X[C.idx(sc, tcu)] +
-            wa * vb * X[C.idx(sc + 1, tc)] + wa * va * X[C.idx(sc + 1, tcu)];
+        v = wb * vb * ldv<CG>(X + C.idx(sc, tc)) + wb * va * ldv<CG>(X + C.idx(sc, tcu)) +
+            wa * vb * ldv<CG>(X + C.idx(sc + 1, tc)) + wa * va * ldv<CG>(X + C.idx(sc + 1, tcu));
     }
     if (ADD)
-        Y[p] += v;
+        Y[p] = ldv<CG>(Y + p) + v;
     else
         Y[p] = v;
 }
@@ -1563,6 +1588,7 @@ __global__ void __launch_bounds__(256) k_prolong(LevelView F, LevelView C, Weigh
                                                  const double* __restrict__ cu,
                                                  double* __restrict__ fu,
                                                  const int* __restrict__ active) {
+    pdl_enter();
     const int b = blockIdx.y;
     if (active && !active[b]) return;
     const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1594,6 +1620,7 @@ __device__ __forceinline__ void env_solve(const EnvFactor& E, int b, double* __r
 // (multigrid.cpp:183-187, line_algebra.cpp:211-255), one thread per section.
 __global__ void k_coarse(EnvFactor E, const double* __restrict__ f, double* __restrict__ u,
                          int B, const int* __restrict__ active) {
+    pdl_enter();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B || (active && !active[b])) return;
     double* x = u + (long)b * E.n;
@@ -1748,23 +1775,25 @@ __device__ __forceinline__ void warp_line_solve(double (&y)[KW], const double* _
 // section's [10][n] block): absent couplings are stored as 0 and their
 // neighbour index is the node itself, so every row is the same 10 products.
 // rhs of circle row (s,t): f - sum of the off-line couplings (smoother.cpp:162-182)
+template <bool CG>
 __device__ __forceinline__ double circle_rhs(const LevelView& L, const double* __restrict__ Rw,
                                              const double* __restrict__ U,
                                              const double* __restrict__ F, int s, int t) {
     const int p = s * L.nt + t, n = L.n;
     const Nbr q = neighbours(L, s, t, p);
-    double acc = F[p];
-    acc -= Rw[1 * n + p] * U[q.pSM];
-    acc -= Rw[2 * n + p] * U[q.pSP];
-    acc -= Rw[5 * n + p] * U[q.pSMTM];
-    acc -= Rw[6 * n + p] * U[q.pSMTP];
-    acc -= Rw[7 * n + p] * U[q.pSPTM];
-    acc -= Rw[8 * n + p] * U[q.pSPTP];
+    double acc = ldv<CG>(F + (p));
+    acc -= Rw[1 * n + p] * ldv<CG>(U + (q.pSM));
+    acc -= Rw[2 * n + p] * ldv<CG>(U + (q.pSP));
+    acc -= Rw[5 * n + p] * ldv<CG>(U + (q.pSMTM));
+    acc -= Rw[6 * n + p] * ldv<CG>(U + (q.pSMTP));
+    acc -= Rw[7 * n + p] * ldv<CG>(U + (q.pSPTM));
+    acc -= Rw[8 * n + p] * ldv<CG>(U + (q.pSPTP));
     return acc;
 }
 
 // r = f - A u of node p with the assembled row (apply_take order,
 // stencil.cpp:166-171)
+template <bool CG>
 __device__ __forceinline__ double row_residual(const LevelView& L, const double* __restrict__ Rw,
                                                const double* __restrict__ U,
                                                const double* __restrict__ F, int p) {
@@ -1775,21 +1804,21 @@ __device__ __forceinline__ double row_residual(const LevelView& L, const double*
     int pph = p;
     if (s == 0 && L.boundary == 0) pph = t + L.nt / 2 >= L.nt ? t + L.nt / 2 - L.nt : t + L.nt / 2;
     double acc = 0.0;
-    acc += Rw[p] * U[p];
-    acc += Rw[1 * n + p] * U[q.pSM];
-    acc += Rw[2 * n + p] * U[q.pSP];
-    acc += Rw[3 * n + p] * U[q.pTM];
-    acc += Rw[4 * n + p] * U[q.pTP];
-    acc += Rw[5 * n + p] * U[q.pSMTM];
-    acc += Rw[6 * n + p] * U[q.pSMTP];
-    acc += Rw[7 * n + p] * U[q.pSPTM];
-    acc += Rw[8 * n + p] * U[q.pSPTP];
-    acc += Rw[9 * n + p] * U[pph];
-    return F[p] - acc;
+    acc += Rw[p] * ldv<CG>(U + (p));
+    acc += Rw[1 * n + p] * ldv<CG>(U + (q.pSM));
+    acc += Rw[2 * n + p] * ldv<CG>(U + (q.pSP));
+    acc += Rw[3 * n + p] * ldv<CG>(U + (q.pTM));
+    acc += Rw[4 * n + p] * ldv<CG>(U + (q.pTP));
+    acc += Rw[5 * n + p] * ldv<CG>(U + (q.pSMTM));
+    acc += Rw[6 * n + p] * ldv<CG>(U + (q.pSMTP));
+    acc += Rw[7 * n + p] * ldv<CG>(U + (q.pSPTM));
+    acc += Rw[8 * n + p] * ldv<CG>(U + (q.pSPTP));
+    acc += Rw[9 * n + p] * ldv<CG>(U + (pph));
+    return ldv<CG>(F + (p)) - acc;
 }
 
 // warp version of origin_solve (2nd-order recurrences as 2x2-map scans)
-template <int KW>
+template <int KW, bool CG>
 __device__ void origin_warp(const CoarseLevel& C, double* __restrict__ U,
                             const double* __restrict__ F, long off, int b) {
     const LevelView& L = C.v;
@@ -1809,7 +1838,7 @@ __device__ void origin_warp(const CoarseLevel& C, double* __restrict__ U,
     for (int q = 0; q < KW; ++q) {
         const int i = j0 + q;
         const bool in = q < KE;
-        x[q] = (in && i < n) ? circle_rhs(L, Rw, U, F, 0, operm(i, h)) : 0.0;
+        x[q] = (in && i < n) ? circle_rhs<CG>(L, Rw, U, F, 0, operm(i, h)) : 0.0;
         if (in && i < nb) {
             const double l1 = i >= 1 ? b1[i] : 0.0, l2 = i >= 2 ? b2[i] : 0.0;
             const Map2 mi = {0.0, 1.0, -l2, -l1, 0.0, x[q]};
@@ -1892,13 +1921,13 @@ __device__ void origin_warp(const CoarseLevel& C, double* __restrict__ U,
     }
 }
 
-template <int KW>
-__device__ void coarse_smooth(const CoarseLevel& C, int b) {
+template <int KW, bool CG, class Team>
+__device__ void coarse_smooth(const CoarseLevel& C, int b, const Team& team) {
     const LevelView& L = C.v;
     const long off = (long)b * L.n;
     double* U = C.u + off;
     const double* F = C.f + off;
-    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
+    const int warp = team.warp(), nw = team.nwarps(), lane = threadIdx.x & 31;
     const int nt = L.nt;
     const double* Rw = C.rows + (long)b * 10 * L.n;
     for (int parity = 0; parity < 2; ++parity) {  // circle sweeps (smoother.cpp:95-116)
@@ -1906,11 +1935,11 @@ __device__ void coarse_smooth(const CoarseLevel& C, int b) {
         for (int li = warp; li < lines; li += nw) {
             const int s = parity + 2 * li;
             if (L.dir(s)) {
-                for (int t = lane; t < nt; t += 32) U[s * nt + t] = F[s * nt + t];
+                for (int t = lane; t < nt; t += 32) U[s * nt + t] = ldv<CG>(F + (s * nt + t));
                 continue;
             }
             if (s == 0 && L.boundary == 0) {
-                origin_warp<KW>(C, U, F, off, b);
+                origin_warp<KW, CG>(C, U, F, off, b);
                 continue;
             }
             double y[KW];
@@ -1918,7 +1947,7 @@ __device__ void coarse_smooth(const CoarseLevel& C, int b) {
             const int j0 = lane * KE;
 #pragma unroll
             for (int q = 0; q < KW; ++q)
-                y[q] = (q < KE && j0 + q < nt) ? circle_rhs(L, Rw, U, F, s, j0 + q) : 0.0;
+                y[q] = (q < KE && j0 + q < nt) ? circle_rhs<CG>(L, Rw, U, F, s, j0 + q) : 0.0;
             const long fo = (long)b * L.split * nt + (long)s * nt;
             warp_line_solve<true, KW>(y, C.cl + fo, C.cm + fo, nt, C.corner[(long)b * L.split + s]);
             __syncwarp();
@@ -1926,7 +1955,7 @@ __device__ void coarse_smooth(const CoarseLevel& C, int b) {
             for (int q = 0; q < KW; ++q)
                 if (q < KE && j0 + q < nt) U[s * nt + j0 + q] = y[q];
         }
-        __syncthreads();
+        team.sync();
     }
     if (L.len <= 0) return;
     const int n = L.n;
@@ -1945,14 +1974,14 @@ __device__ void coarse_smooth(const CoarseLevel& C, int b) {
                 if (q < KE && i < L.len) {
                     const int p = base + i;
                     const Nbr nb = neighbours(L, s, t, p);
-                    acc = F[p];
-                    if (s == L.split) acc -= Rw[1 * n + p] * U[nb.pSM];
-                    acc -= Rw[3 * n + p] * U[nb.pTM];
-                    acc -= Rw[4 * n + p] * U[nb.pTP];
-                    acc -= Rw[5 * n + p] * U[nb.pSMTM];
-                    acc -= Rw[6 * n + p] * U[nb.pSMTP];
-                    acc -= Rw[7 * n + p] * U[nb.pSPTM];
-                    acc -= Rw[8 * n + p] * U[nb.pSPTP];
+                    acc = ldv<CG>(F + (p));
+                    if (s == L.split) acc -= Rw[1 * n + p] * ldv<CG>(U + (nb.pSM));
+                    acc -= Rw[3 * n + p] * ldv<CG>(U + (nb.pTM));
+                    acc -= Rw[4 * n + p] * ldv<CG>(U + (nb.pTP));
+                    acc -= Rw[5 * n + p] * ldv<CG>(U + (nb.pSMTM));
+                    acc -= Rw[6 * n + p] * ldv<CG>(U + (nb.pSMTP));
+                    acc -= Rw[7 * n + p] * ldv<CG>(U + (nb.pSPTM));
+                    acc -= Rw[8 * n + p] * ldv<CG>(U + (nb.pSPTP));
                 }
                 y[q] = acc;
             }
@@ -1963,7 +1992,7 @@ __device__ void coarse_smooth(const CoarseLevel& C, int b) {
             for (int q = 0; q < KW; ++q)
                 if (q < KE && j0 + q < L.len) U[base + j0 + q] = y[q];
         }
-        __syncthreads();
+        team.sync();
     }
 }
 
@@ -2005,81 +2034,90 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-// Executes the op program; `bb` is the section index used for per-section
-// arrays (0 when the data is shared-memory resident and section-sliced).
-template <int KW>
-__device__ __forceinline__ void run_prog(const CoarseLevel* lv, const EnvFactor& env,
-                                         const int* __restrict__ prog, int nops, int bb,
-                                         unsigned long long* trace = nullptr) {
-    for (int i = 0; i < nops; ++i) {
-        const int op = prog[i] & 255, l = prog[i] >> 8;
-        const CoarseLevel& C = lv[l];
-        const long off = (long)bb * C.v.n;
-        switch (op) {
-            case OP_SMOOTH:
-                coarse_smooth<KW>(C, bb);
-                break;
-            case OP_RESIDUAL:
-                for (int p = threadIdx.x; p < C.v.n; p += blockDim.x)
-                    C.res[off + p] =
-                        row_residual(C.v, C.rows + (long)bb * 10 * C.v.n, C.u + off, C.f + off, p);
-                break;
-            case OP_RESTRICT: {
-                const CoarseLevel& D = lv[l + 1];
-                const long offc = (long)bb * D.v.n;
-                for (int p = threadIdx.x; p < D.v.n; p += blockDim.x)
-                    restrict_node(C.v, D.v, C.w, C.res + off, D.f + offc, D.u + offc, 1, p);
-                break;
-            }
-            case OP_PROLONG: {
-                const CoarseLevel& D = lv[l + 1];
-                const long offc = (long)bb * D.v.n;
-                for (int p = threadIdx.x; p < C.v.n; p += blockDim.x)
-                    prolong_node<true>(C.v, D.v, C.w, D.u + offc, C.u + off, p);
-                break;
-            }
-            default: {  // OP_COARSE: u = f, envelope LDL^T (multigrid.cpp:183-187)
-                if (env.inv) {  // dense inverse: one row per thread
-                    const int n = env.n;
-                    const double* A = env.inv + (long)bb * n * n;
-                    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-                        double a0 = 0.0, a1 = 0.0;
-                        int j = 0;
-                        for (; j + 1 < n; j += 2) {
-                            a0 += A[(long)j * n + i] * C.f[off + j];
-                            a1 += A[(long)(j + 1) * n + i] * C.f[off + j + 1];
-                        }
-                        if (j < n) a0 += A[(long)j * n + i] * C.f[off + j];
-                        C.u[off + i] = a0 + a1;
-                    }
-                } else if (threadIdx.x == 0) {
-                    double* x = C.u + off;
-                    for (int k = 0; k < env.n; ++k) x[k] = C.f[off + k];
-                    env_solve(env, bb, x);
-                }
-                break;
-            }
+// Who executes a phase: one block (the resident tail) or every block of a
+// thread-block cluster (the cluster-wide multigrid kernel).
+struct BlockTeam {
+    __device__ int warp() const { return threadIdx.x >> 5; }
+    __device__ int nwarps() const { return blockDim.x >> 5; }
+    __device__ int tid() const { return threadIdx.x; }
+    __device__ int nthreads() const { return blockDim.x; }
+    __device__ void sync() const { __syncthreads(); }
+};
+struct ClusterTeam {
+    int rank, size;
+    // consecutive lines go to different CTAs (SMs)
+    __device__ int warp() const { return (threadIdx.x >> 5) * size + rank; }
+    __device__ int nwarps() const { return size * (blockDim.x >> 5); }
+    __device__ int tid() const { return rank * blockDim.x + threadIdx.x; }
+    __device__ int nthreads() const { return size * blockDim.x; }
+    __device__ void sync() const { cg::this_cluster().sync(); }
+};
+
+// One op of a program on level C (D = level below for transfers); `bb` is
+// the section index of the per-section arrays (0 when shared-memory resident).
+template <int KW, bool CG, class Team>
+__device__ __forceinline__ void exec_op(int op, const CoarseLevel& C, const CoarseLevel& D,
+                                        const EnvFactor& env, int bb, const Team& team) {
+    const long off = (long)bb * C.v.n;
+    switch (op) {
+        case OP_SMOOTH:
+            coarse_smooth<KW, CG>(C, bb, team);
+            break;
+        case OP_RESIDUAL:
+            for (int p = team.tid(); p < C.v.n; p += team.nthreads())
+                C.res[off + p] =
+                    row_residual<CG>(C.v, C.rows + (long)bb * 10 * C.v.n, C.u + off, C.f + off, p);
+            break;
+        case OP_RESTRICT: {
+            const long offc = (long)bb * D.v.n;
+            for (int p = team.tid(); p < D.v.n; p += team.nthreads())
+                restrict_node<CG>(C.v, D.v, C.w, C.res + off, D.f + offc, D.u + offc, 1, p);
+            break;
         }
-        __syncthreads();
-        if (trace && threadIdx.x == 0) trace[2 + i] = globaltimer();
+        case OP_PROLONG: {
+            const long offc = (long)bb * D.v.n;
+            for (int p = team.tid(); p < C.v.n; p += team.nthreads())
+                prolong_node<true, CG>(C.v, D.v, C.w, D.u + offc, C.u + off, p);
+            break;
+        }
+        default: {  // OP_COARSE: u = f, envelope LDL^T (multigrid.cpp:183-187)
+            if (env.inv) {  // dense inverse: one row per thread
+                const int n = env.n;
+                const double* A = env.inv + (long)bb * n * n;
+                for (int i = team.tid(); i < n; i += team.nthreads()) {
+                    double a0 = 0.0, a1 = 0.0;
+                    int j = 0;
+                    for (; j + 1 < n; j += 2) {
+                        a0 += A[(long)j * n + i] * C.f[off + j];
+                        a1 += A[(long)(j + 1) * n + i] * C.f[off + j + 1];
+                    }
+                    if (j < n) a0 += A[(long)j * n + i] * C.f[off + j];
+                    C.u[off + i] = a0 + a1;
+                }
+            } else if (team.tid() == 0) {
+                double* x = C.u + off;
+                for (int k = 0; k < env.n; ++k) x[k] = C.f[off + k];
+                env_solve(env, bb, x);
+            }
+            break;
+        }
     }
 }
 
+// The resident tail of section b, run by one block: stage this section's
+// slice of every tail array into shared memory, run the op program, write the
+// top level's correction back.
+// (one instance per kernel, shared by the tail_body instantiations)
+__shared__ __align__(16) TailImage simg;
+__shared__ __align__(8) unsigned long long sbar;
+__shared__ unsigned stx;
+
 template <int KW>
-__global__ void __launch_bounds__(512) k_coarse_cycle(const __grid_constant__ CoarseParams cp,
-                                                      const int* __restrict__ prog, int nops,
-                                                      const int* __restrict__ active) {
+__device__ void tail_body(const CoarseParams& cp, const int* __restrict__ prog, int nops, int b,
+                          unsigned long long* trace) {
     extern __shared__ __align__(16) char sbuf[];
-    __shared__ __align__(16) TailImage simg;
-    const int b = blockIdx.x;
-    if (active && !active[b]) return;
-    unsigned long long* trace = b == 0 ? cp.trace : nullptr;
-    if (trace && threadIdx.x == 0) trace[0] = globaltimer();
-    // stage this section's slice of every tail array into shared memory: one
-    // thread per array issues a bulk (TMA) copy of its 16-byte aligned part,
-    // completing on an mbarrier; leftovers go through cp.async
-    __shared__ __align__(8) unsigned long long sbar;
-    __shared__ unsigned stx;
+    // one thread per array issues a bulk (TMA) copy of its 16-byte aligned
+    // part, completing on an mbarrier; leftovers go through cp.async
     if (threadIdx.x == 0) {
         mbar_init(&sbar, 1);
         stx = 0;
@@ -2117,17 +2155,86 @@ __global__ void __launch_bounds__(512) k_coarse_cycle(const __grid_constant__ Co
     if (trace && threadIdx.x == 0) trace[nops + 3] = globaltimer();
     __syncthreads();
     if (trace && threadIdx.x == 0) trace[1] = globaltimer();
-    run_prog<KW>(simg.lv - cp.first, simg.env, prog, nops, 0, trace);
+    const CoarseLevel* lv = simg.lv - cp.first;
+    const BlockTeam team;
+    for (int i = 0; i < nops; ++i) {
+        const int op = prog[i] & 255, l = prog[i] >> 8;
+        exec_op<KW, false>(op, lv[l], lv[l + (op == OP_COARSE ? 0 : 1)], simg.env, 0, team);
+        __syncthreads();
+        if (trace && threadIdx.x == 0) trace[2 + i] = globaltimer();
+    }
     // the top level's correction goes back to global memory
     const CoarseLevel& top = simg.lv[0];
     for (int p = threadIdx.x; p < top.v.n; p += blockDim.x)
         cp.top_u_global[(long)b * top.v.n + p] = top.u[p];
 }
 
+template <int KW>
+__global__ void __launch_bounds__(512) k_coarse_cycle(const __grid_constant__ CoarseParams cp,
+                                                      const int* __restrict__ prog, int nops,
+                                                      const int* __restrict__ active) {
+    pdl_enter();
+    const int b = blockIdx.x;
+    if (active && !active[b]) return;
+    unsigned long long* trace = b == 0 ? cp.trace : nullptr;
+    if (trace && threadIdx.x == 0) trace[0] = globaltimer();
+    tail_body<KW>(cp, prog, nops, b, trace);
+}
+
+__device__ __forceinline__ void tail_dispatch(const CoarseParams& cp, const int* prog, int nops,
+                                              int b) {
+    switch (cp.kw) {
+        case 1: tail_body<1>(cp, prog, nops, b, nullptr); break;
+        case 2: tail_body<2>(cp, prog, nops, b, nullptr); break;
+        case 4: tail_body<4>(cp, prog, nops, b, nullptr); break;
+        default: tail_body<8>(cp, prog, nops, b, nullptr); break;
+    }
+}
+
+// Cluster-wide multigrid sub-cycle: the levels between the level kernels and
+// the resident tail run in ONE launch, one thread-block cluster per section;
+// every phase is spread over all warps / threads of the cluster and followed
+// by a cluster barrier (instead of a kernel boundary).  Vectors written inside
+// the launch are read with ld.global.cg.  OP_TAIL: block 0 runs the resident
+// tail (tail_body) while the others wait at the barrier.
+__global__ void __launch_bounds__(512) k_mid_cycle(const __grid_constant__ MidParams mp,
+                                                   const int* __restrict__ prog, int nops,
+                                                   const int* __restrict__ active) {
+    pdl_enter();
+    cg::cluster_group cluster = cg::this_cluster();
+    const int b = blockIdx.x / mp.cl;
+    if (active && !active[b]) return;  // uniform over the cluster
+    const ClusterTeam team{static_cast<int>(cluster.block_rank()), mp.cl};
+    unsigned long long* trace = (b == 0 && team.rank == 0 && threadIdx.x == 0) ? mp.trace : nullptr;
+    if (trace) trace[0] = globaltimer();
+    for (int i = 0; i < nops; ++i) {
+        const int op = prog[i] & 255, l = prog[i] >> 8;
+        if (op == OP_TAIL) {
+            if (team.rank == 0) {
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                tail_dispatch(mp.tail, mp.tprog[l], mp.tlen[l], b);
+            }
+        } else {
+            const int k = l - mp.first;
+            const CoarseLevel& C = mp.lv[k];
+            const CoarseLevel& D = mp.lv[k + 1];
+            switch (mp.kw[k]) {
+                case 1: exec_op<1, true>(op, C, D, mp.tail.env, b, team); break;
+                case 2: exec_op<2, true>(op, C, D, mp.tail.env, b, team); break;
+                case 4: exec_op<4, true>(op, C, D, mp.tail.env, b, team); break;
+                default: exec_op<8, true>(op, C, D, mp.tail.env, b, team); break;
+            }
+        }
+        cluster.sync();
+        if (trace) trace[1 + i] = globaltimer();
+    }
+}
+
 // ------------------------------------------------------------------- norms
 __global__ void __launch_bounds__(256) k_norm_partials(const double* __restrict__ v, long n,
                                                        int norm_type,
                                                        double* __restrict__ partials) {
+    pdl_enter();
     const int b = blockIdx.y;
     const double* V = v + (long)b * n;
     double a = 0.0;
@@ -2156,6 +2263,7 @@ __global__ void __launch_bounds__(256) k_norm_partials(const double* __restrict_
 __global__ void __launch_bounds__(256) k_norm_final(const double* __restrict__ partials,
                                                     int nblk, long n, int norm_type,
                                                     double* __restrict__ norms) {
+    pdl_enter();
     const int b = blockIdx.x;
     double a = 0.0;
     for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
@@ -2185,6 +2293,7 @@ __global__ void __launch_bounds__(256) k_norm_final(const double* __restrict__ p
 // convergence test of MultigridSolver::solve (multigrid.cpp:321-340)
 __global__ void k_check(const double* __restrict__ norms, ConvState cs, int B, int max_it,
                         double rel_tol, double abs_tol) {
+    pdl_enter();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B || !cs.active[b]) return;
     const int it = cs.count[b]++;  // residual norms taken so far = iteration index
@@ -2206,12 +2315,14 @@ __global__ void k_check(const double* __restrict__ norms, ConvState cs, int B, i
 }
 
 __global__ void k_fill(double* p, long n, double v) {
+    pdl_enter();
     for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long)gridDim.x * blockDim.x)
         p[i] = v;
 }
 
 __global__ void k_set_active(int* active, int* count, int* conv, int* remaining, int B) {
+    pdl_enter();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b < B) {
         active[b] = 1;
@@ -2266,6 +2377,31 @@ inline size_t line_smem(int n) { return (size_t)(3 * padded(n) + 32 * 6 + 16) * 
 
 }  // namespace
 
+// Launch with programmatic stream serialization (PDL) when PMG_PDL=1 (off by
+// default: no measurable gain inside the replayed cycle graph, r01).
+static bool pdl_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("PMG_PDL");
+        return e ? std::atoi(e) != 0 : false;
+    }();
+    return on;
+}
+template <class... KArgs, class... Args>
+static void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_on() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 int apply_launches(const LevelView& L) { return 1; }
 
 int apply_blocks(const LevelView& L) { return tile_geom(L).ntiles(); }
@@ -2278,7 +2414,7 @@ int launch_apply(const LevelView& L, bool onfly, int mode, const double* u, cons
     dim3 grid(nb, L.B);
     const bool norm = partials != nullptr;
 #define PMG_APPLY(ON, MO, NO) \
-    k_apply_tiled<ON, MO, NO><<<grid, 256, 0, st>>>(L, G, u, f, out, partials, norm_type, active)
+    launch_k(k_apply_tiled<ON, MO, NO>, grid, 256, 0, st, L, G, u, f, out, partials, norm_type, active)
     if (onfly) {
         if (mode == 0) {
             if (norm) PMG_APPLY(true, 0, true); else PMG_APPLY(true, 0, false);
@@ -2303,7 +2439,7 @@ static void circle_k(const LevelView& L, double* u, const double* f, const doubl
                      const int* active, cudaStream_t st, int T, int lines) {
     const size_t sm = line_smem(L.nt);
     set_smem(k_circle<ON, K>, sm);
-    k_circle<ON, K><<<dim3(lines, L.B), T, sm, st>>>(L, u, f, cil, cm, corner, cz, of, parity,
+    launch_k(k_circle<ON, K>, dim3(lines, L.B), T, sm, st, L, u, f, cil, cm, corner, cz, of, parity,
                                                       serial ? 1 : 0, exact_rings, active);
 }
 
@@ -2327,13 +2463,15 @@ static void launch_cluster(Kern kern, int C, dim3 grid, int T, size_t smem, cuda
     cfg.blockDim = dim3(T, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = C;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_on() ? 2 : 1;
     cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
@@ -2457,7 +2595,7 @@ static void radial_k(const LevelView& L, double* u, const double* f, const doubl
                      cudaStream_t st, int T, int lines) {
     const size_t sm = line_smem(L.len);
     set_smem(k_radial<ON, K>, sm);
-    k_radial<ON, K><<<dim3(lines, L.B), T, sm, st>>>(L, u, f, ril, rm, parity, serial ? 1 : 0,
+    launch_k(k_radial<ON, K>, dim3(lines, L.B), T, sm, st, L, u, f, ril, rm, parity, serial ? 1 : 0,
                                                       active);
 }
 
@@ -2502,7 +2640,7 @@ void launch_radial(const LevelView& L, bool onfly, double* u, const double* f, c
 
 void launch_restrict(const LevelView& F, const LevelView& C, const Weights& w, const double* fr,
                      double* cf, double* cu_zero, bool mask, const int* active, cudaStream_t st) {
-    k_restrict<<<dim3((C.n + 255) / 256, C.B), 256, 0, st>>>(F, C, w, fr, cf, cu_zero, mask ? 1 : 0,
+    launch_k(k_restrict, dim3((C.n + 255) / 256, C.B), 256, 0, st, F, C, w, fr, cf, cu_zero, mask ? 1 : 0,
                                                              active);
 }
 
@@ -2510,44 +2648,44 @@ void launch_prolong(const LevelView& F, const LevelView& C, const Weights& w, co
                     double* fu, bool add, const int* active, cudaStream_t st) {
     dim3 grid((F.n + 255) / 256, F.B);
     if (add)
-        k_prolong<true><<<grid, 256, 0, st>>>(F, C, w, cu, fu, active);
+        launch_k(k_prolong<true>, grid, 256, 0, st, F, C, w, cu, fu, active);
     else
-        k_prolong<false><<<grid, 256, 0, st>>>(F, C, w, cu, fu, active);
+        launch_k(k_prolong<false>, grid, 256, 0, st, F, C, w, cu, fu, active);
 }
 
 void launch_coarse(const LevelView& L, const EnvFactor& E, const double* f, double* u,
                    const int* active, cudaStream_t st) {
-    k_coarse<<<(L.B + 63) / 64, 64, 0, st>>>(E, f, u, L.B, active);
+    launch_k(k_coarse, (L.B + 63) / 64, 64, 0, st, E, f, u, L.B, active);
 }
 
 int launch_norm_partials(const double* v, long n, int B, int norm_type, double* partials,
                          cudaStream_t st) {
     long nb = (n + 255) / 256;
     if (nb > 1024) nb = 1024;
-    k_norm_partials<<<dim3((int)nb, B), 256, 0, st>>>(v, n, norm_type, partials);
+    launch_k(k_norm_partials, dim3((int)nb, B), 256, 0, st, v, n, norm_type, partials);
     return (int)nb;
 }
 
 void launch_norm_final(const double* partials, int nblk, int B, long n, int norm_type,
                        double* norms, cudaStream_t st) {
-    k_norm_final<<<B, 256, 0, st>>>(partials, nblk, n, norm_type, norms);
+    launch_k(k_norm_final, B, 256, 0, st, partials, nblk, n, norm_type, norms);
 }
 
 void launch_check(const double* norms, ConvState cs, int B, int max_it, double rel_tol,
                   double abs_tol, cudaStream_t st) {
-    k_check<<<(B + 127) / 128, 128, 0, st>>>(norms, cs, B, max_it, rel_tol, abs_tol);
+    launch_k(k_check, (B + 127) / 128, 128, 0, st, norms, cs, B, max_it, rel_tol, abs_tol);
 }
 
 void launch_fill(double* p, long n, double v, cudaStream_t st) {
     long nb = (n + 255) / 256;
     if (nb > 4096) nb = 4096;
     if (nb < 1) nb = 1;
-    k_fill<<<(int)nb, 256, 0, st>>>(p, n, v);
+    launch_k(k_fill, (int)nb, 256, 0, st, p, n, v);
 }
 
 void launch_set_active(int* active, int* count, int* conv, int* remaining, int B,
                        cudaStream_t st) {
-    k_set_active<<<(B + 127) / 128, 128, 0, st>>>(active, count, conv, remaining, B);
+    launch_k(k_set_active, (B + 127) / 128, 128, 0, st, active, count, conv, remaining, B);
 }
 
 void launch_flush(double* buf, long n, cudaStream_t st) {
@@ -2557,6 +2695,60 @@ void launch_flush(double* buf, long n, cudaStream_t st) {
 }  // namespace pmg
 
 namespace pmg {
+void launch_mid_cycle(const MidParams& mp, const int* prog, int nops, int B, const int* active,
+                      cudaStream_t st) {
+    const size_t sm = (size_t)mp.tail.smem_bytes;
+    set_smem(k_mid_cycle, sm);
+    static std::set<int> nonportable;
+    {
+        static std::mutex mu;
+        std::lock_guard<std::mutex> g(mu);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (!nonportable.count(dev)) {
+            cudaFuncSetAttribute(k_mid_cycle, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            nonportable.insert(dev);
+        }
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(mp.cl * B);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = mp.cl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_on() ? 2 : 1;
+    cudaLaunchKernelEx(&cfg, k_mid_cycle, mp, prog, nops, active);
+}
+
+int mid_cluster_size(size_t smem, int want) {
+    set_smem(k_mid_cycle, smem);
+    cudaFuncSetAttribute(k_mid_cycle, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (int c = want; c >= 2; c /= 2) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(c);
+        cfg.blockDim = dim3(512);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = c;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k_mid_cycle, &cfg) == cudaSuccess && n > 0) return c;
+        cudaGetLastError();
+    }
+    return 0;
+}
+
 void launch_coarse_cycle(const CoarseParams& cp, const int* prog, int nops, int B, bool onfly,
                          const int* active, cudaStream_t st) {
     (void)onfly;  // the tail evaluates assembled rows in both stencil modes
@@ -2564,19 +2756,19 @@ void launch_coarse_cycle(const CoarseParams& cp, const int* prog, int nops, int 
     switch (cp.kw) {
         case 1:
             set_smem(k_coarse_cycle<1>, sm);
-            k_coarse_cycle<1><<<B, 512, sm, st>>>(cp, prog, nops, active);
+            launch_k(k_coarse_cycle<1>, B, 512, sm, st, cp, prog, nops, active);
             break;
         case 2:
             set_smem(k_coarse_cycle<2>, sm);
-            k_coarse_cycle<2><<<B, 512, sm, st>>>(cp, prog, nops, active);
+            launch_k(k_coarse_cycle<2>, B, 512, sm, st, cp, prog, nops, active);
             break;
         case 4:
             set_smem(k_coarse_cycle<4>, sm);
-            k_coarse_cycle<4><<<B, 512, sm, st>>>(cp, prog, nops, active);
+            launch_k(k_coarse_cycle<4>, B, 512, sm, st, cp, prog, nops, active);
             break;
         default:
             set_smem(k_coarse_cycle<8>, sm);
-            k_coarse_cycle<8><<<B, 512, sm, st>>>(cp, prog, nops, active);
+            launch_k(k_coarse_cycle<8>, B, 512, sm, st, cp, prog, nops, active);
             break;
     }
 }

@@ -48,7 +48,14 @@ struct CoarseLevel {
     Weights w;  // this level as the fine level of a transfer
 };
 
-enum CoarseOp { OP_SMOOTH = 0, OP_RESIDUAL = 1, OP_RESTRICT = 2, OP_PROLONG = 3, OP_COARSE = 4 };
+enum CoarseOp {
+    OP_SMOOTH = 0,
+    OP_RESIDUAL = 1,
+    OP_RESTRICT = 2,
+    OP_PROLONG = 3,
+    OP_COARSE = 4,
+    OP_TAIL = 5  // cluster kernel: run the resident tail program of cycle type (op >> 8)
+};
 
 // Level descriptors of the coarse tail passed BY VALUE (constant bank):
 // lv[i] describes level first + i.
@@ -88,6 +95,24 @@ struct CoarseParams {
     // staging and after every op; null = off
     unsigned long long* trace;
 };
+
+// Levels between the level kernels and the resident tail, run by one
+// thread-block cluster per section (global memory, L2-resident).
+constexpr int kMaxMid = 8;
+struct MidParams {
+    CoarseLevel lv[kMaxMid + 1];  // lv[i] = level first + i (global pointers); lv[nmid] = tail top
+    int kw[kMaxMid];              // rows per lane of level first + i
+    int first, nmid;
+    int cl;                       // cluster size
+    const int* tprog[3];          // resident tail programs per cycle type
+    int tlen[3];
+    CoarseParams tail;
+    unsigned long long* trace;  // PMG_TAIL_TRACE: %globaltimer per op (cluster 0, rank 0)
+};
+void launch_mid_cycle(const MidParams& mp, const int* prog, int nops, int B, const int* active,
+                      cudaStream_t st);
+// largest cluster size <= want (power of 2) that can be scheduled, 0 if none
+int mid_cluster_size(size_t smem, int want);
 
 // Runs an op program (op | level << 8) over the coarse levels, one block per
 // section.

@@ -211,6 +211,10 @@ struct Solver {
     int* d_prog[3] = {nullptr, nullptr, nullptr};
     int prog_len[3] = {0, 0, 0};
     std::vector<int> h_prog[3];
+    MidParams mid_params{};
+    int mid_start = -1;
+    int* d_mprog[3] = {nullptr, nullptr, nullptr};
+    int mprog_len[3] = {0, 0, 0};
     // CUDA graph of one cycle + residual norm + convergence check
     cudaGraphExec_t cycle_exec = nullptr;
     long long cycle_nodes = 0;
@@ -337,6 +341,7 @@ struct Solver {
             setup_level(V, l == L - 1, bad);
         }
         setup_coarse_tail();
+        setup_mid();
         // convergence state
         hist_cap = std::max(set.max_iterations, 0) + 1;
         norms = alloc<double>(B);
@@ -677,6 +682,127 @@ struct Solver {
             coarse_params.trace = alloc<unsigned long long>(maxlen + 4);
     }
 
+    // Cluster-wide sub-cycle (k_mid_cycle): the levels just above the resident
+    // tail whose lines fit a warp and whose vectors stay in L2 run in one
+    // launch per cycle, one thread-block cluster per section.
+    void setup_mid() {
+        if (coarse_start <= 0 || serial) return;
+        long max_nodes = 5000;
+        if (const char* e = std::getenv("PMG_MID_NODES")) max_nodes = std::atol(e);
+        int max_b = 16;
+        if (const char* e = std::getenv("PMG_MID_SECTIONS")) max_b = std::atoi(e);
+        if (max_nodes <= 0 || B > max_b) return;
+        int first = coarse_start;
+        while (first - 1 >= 0 && coarse_start - (first - 1) <= kMaxMid) {
+            const HostGrid& g = lv[first - 1].g;
+            if (!(g.nt() <= 256 && g.nr() - g.split <= 256 && g.uniform_angles &&
+                  g.n() <= max_nodes))
+                break;
+            --first;
+        }
+        if (first == coarse_start) return;
+        int want = 16;
+        if (const char* e = std::getenv("PMG_MID_CLUSTER")) want = std::atoi(e);
+        const int cl = mid_cluster_size((size_t)coarse_params.smem_bytes, want);
+        if (cl < 2) return;
+        std::memset(&mid_params, 0, sizeof mid_params);
+        mid_params.first = first;
+        mid_params.nmid = coarse_start - first;
+        mid_params.cl = cl;
+        mid_params.tail = coarse_params;
+        for (int t = 0; t < 3; ++t) {
+            mid_params.tprog[t] = d_prog[t];
+            mid_params.tlen[t] = prog_len[t];
+        }
+        for (int l = first; l <= coarse_start; ++l) {
+            Level& V = lv[l];
+            const HostGrid& g = V.g;
+            const long n = g.n();
+            CoarseLevel& c = mid_params.lv[l - first];
+            c.v = V.v;
+            c.u = V.u;
+            c.f = V.f;
+            if (l == coarse_start) break;  // tail top: restrict target / prolong source
+            c.res = V.res;
+            c.cl = V.cil;
+            c.cm = V.cm;
+            c.corner = V.corner;
+            c.rl = V.ril;
+            c.rm = V.rm;
+            if (!V.rows) {
+                V.rows = alloc<double>((size_t)B * 10 * n, false);
+                launch_rows(V.v, onfly, V.rows, stream);
+            }
+            c.rows = V.rows;
+            if (set.boundary_mode == 0) {
+                c.of.band1 = V.ob1;
+                c.of.band2 = V.ob2;
+                c.of.row1 = V.or1;
+                c.of.row2 = V.or2;
+                c.of.D = V.oD;
+                c.of.fc1 = V.ofc1;
+                c.of.fc2 = V.ofc2;
+            }
+            c.w = V.w;
+            int kw = 1;
+            while (32 * kw < std::max(g.nt(), g.nr() - g.split)) kw *= 2;
+            mid_params.kw[l - first] = kw;
+        }
+        for (int type = 0; type < 3; ++type) {
+            std::vector<int> prog;
+            gen_mid_prog(first, type, prog);
+            d_mprog[type] = upload(prog);
+            mprog_len[type] = static_cast<int>(prog.size());
+        }
+        mid_start = first;
+        if (std::getenv("PMG_TAIL_TRACE")) {
+            int mx = 0;
+            for (int t = 0; t < 3; ++t) mx = std::max(mx, mprog_len[t]);
+            mid_params.trace = alloc<unsigned long long>(mx + 1);
+            h_mprog_type = set.cycle;
+            gen_mid_prog(first, set.cycle, h_mprog);
+        }
+    }
+    std::vector<int> h_mprog;
+    int h_mprog_type = 0;
+    void print_mid_trace() {
+        std::vector<unsigned long long> t(h_mprog.size() + 1);
+        PMG_CUDA(cudaMemcpy(t.data(), mid_params.trace, t.size() * 8, cudaMemcpyDeviceToHost));
+        static const char* names[] = {"smooth", "residual", "restrict", "prolong", "coarse", "tail"};
+        double sum[6][kMaxCoarse + 1] = {};
+        for (size_t i = 0; i < h_mprog.size(); ++i) {
+            const int op = h_mprog[i] & 255;
+            const int l = op == OP_TAIL ? kMaxCoarse : (h_mprog[i] >> 8);
+            sum[op][l] += (t[1 + i] - t[i]) * 1e-3;
+        }
+        for (int o = 0; o < 6; ++o)
+            for (int l = 0; l <= kMaxCoarse; ++l)
+                if (sum[o][l] > 0)
+                    std::fprintf(stderr, "mid trace: level %d %-8s %.2f us\n", l, names[o],
+                                 sum[o][l]);
+        std::fprintf(stderr, "mid trace: total %.2f us\n", (t.back() - t[0]) * 1e-3);
+    }
+    void gen_mid_prog(int l, int type, std::vector<int>& prog) const {
+        if (l == coarse_start) {
+            prog.push_back(OP_TAIL | (type << 8));
+            return;
+        }
+        for (int i = 0; i < set.pre_smoothing; ++i) prog.push_back(OP_SMOOTH | (l << 8));
+        prog.push_back(OP_RESIDUAL | (l << 8));
+        prog.push_back(OP_RESTRICT | (l << 8));
+        if (type == 0) {
+            gen_mid_prog(l + 1, 0, prog);
+        } else if (type == 1) {
+            gen_mid_prog(l + 1, 1, prog);
+            gen_mid_prog(l + 1, 1, prog);
+        } else {
+            gen_mid_prog(l + 1, 2, prog);
+            gen_mid_prog(l + 1, 0, prog);
+        }
+        prog.push_back(OP_PROLONG | (l << 8));
+        for (int i = 0; i < set.post_smoothing; ++i) prog.push_back(OP_SMOOTH | (l << 8));
+    }
+
     void release(double* p) {
         auto it = std::find(allocs.begin(), allocs.end(), static_cast<void*>(p));
         if (it != allocs.end()) {
@@ -854,6 +980,12 @@ struct Solver {
     // multigrid.cpp:189-220
     void cycle(int l, int type, const int* act) {
         const int L = static_cast<int>(lv.size());
+        if (l == mid_start) {
+            run(KK_COARSE, 1, [&] {
+                launch_mid_cycle(mid_params, d_mprog[type], mprog_len[type], B, act, stream);
+            });
+            return;
+        }
         if (l == coarse_start) {
             run(KK_COARSE, 1, [&] {
                 launch_coarse_cycle(coarse_params, d_prog[type], prog_len[type], B, onfly, act,
@@ -977,7 +1109,8 @@ struct Solver {
         PMG_CUDA(cudaGetLastError());
         last_solve_ms = ms;
         collect_profile();
-        if (coarse_params.trace) print_tail_trace();
+        if (coarse_params.trace && mid_start < 0) print_tail_trace();
+        if (mid_params.trace) print_mid_trace();
         // reports
         std::vector<int> h_it(B), h_conv(B);
         std::vector<double> h_hist((size_t)B * hist_cap);
