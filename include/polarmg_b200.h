@@ -64,6 +64,8 @@ typedef struct {
     double alpha_jump;
     double delta_r;
     double alpha_scale;
+    int solution;      /* manufactured solution: 0 None (f = 0, u_D = 0), 1 PolarOscillation
+                          (problem.cpp:48-72; make_problem, problem.cpp:150-156) */
 } pmg_problem;
 
 /* Grid construction -- polar_grid.cpp:99-178.
@@ -94,8 +96,10 @@ typedef struct {
     int pre_smoothing, post_smoothing;
     int cycle;             /* 0 V, 1 W, 2 F */
     int extrapolation;     /* must be 0 (not supported yet) */
-    int fmg;               /* must be 0 (not supported yet) */
-    int fmg_iterations, fmg_cycle;
+    int fmg;               /* 1: full-multigrid start (multigrid.cpp:250-265); pmg_solve then
+                              assembles the manufactured RHS of every level (like the
+                              reference's solve()) instead of using the current f */
+    int fmg_iterations, fmg_cycle;  /* cycles per FMG level (>= 1); 0 V, 1 W, 2 F */
     int norm_type;         /* 0 weighted-l2, 1 euclidean, 2 infinity */
     int max_iterations;
     double absolute_tolerance;  /* <= 0 disables */
@@ -120,6 +124,8 @@ typedef struct {
     double setup_seconds;        /* host wall time of pmg_create */
     double solve_seconds;        /* device time (CUDA events) of the solve window */
     size_t device_bytes;         /* all device allocations of the handle */
+    double exact_error_weighted; /* exact_errors() (multigrid.cpp:277-296); -1 without a */
+    double exact_error_infinity; /* manufactured solution */
 } pmg_report;
 
 const char* pmg_last_error(void);
@@ -162,6 +168,18 @@ int pmg_set_rhs_device(pmg_handle h, const void* f_device);
  * canonical order, outer ring zeroed; f = A_take u* computed on the device.
  * If ustar_host is non-NULL it receives u* (layout). */
 int pmg_seeded_rhs(pmg_handle h, unsigned seed, double* ustar_host, int layout);
+
+/* f = the manufactured RHS of the finest level: DiscreteOperator::assemble_rhs
+ * (stencil.cpp:307-353: rhs_f of problem.cpp:108-148 scaled by |det DF| and the
+ * node weight, Dirichlet rows u_D, lifting of Dirichlet couplings), computed on
+ * the device bitwise equal to the reference.  pmg_assemble_rhs + pmg_solve is
+ * the reference's MultigridSolver::solve() (multigrid.cpp:309-316).
+ * PMG_ERUNTIME carries the reference's "rhs_f lost accuracy" / "singular
+ * Jacobian" messages. */
+int pmg_assemble_rhs(pmg_handle h);
+/* exact_errors() of the current finest-level u against the manufactured
+ * solution (multigrid.cpp:277-296), one value per section; -1 without one. */
+int pmg_exact_errors(pmg_handle h, double* weighted, double* infinity);
 
 /* MultigridSolver::solve() with the current RHS.  reports: one per section.
  * history (optional): n_sections * history_cap doubles of residual norms. */

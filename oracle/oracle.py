@@ -70,6 +70,10 @@ class Case:
     abs_tol: float = -1.0
     rel_tol: float = 1e-10
     threads: int = 0
+    solution: int = 0  # 0 None, 1 PolarOscillation (problem.hpp:32-44)
+    fmg: int = 0
+    fmg_iterations: int = 2
+    fmg_cycle: str = "F"
     extra: dict = field(default_factory=dict)
 
     def args(self):
@@ -110,6 +114,11 @@ def _bind(lib, prefix):
     getattr(lib, prefix + "solve").argtypes = [C.c_void_p, _dp, _dp, _dp, _ip, _ip, _dp, _dp]
     getattr(lib, prefix + "row").argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, _ip, _dp, _ip]
     getattr(lib, prefix + "level_coeffs").argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp]
+    getattr(lib, prefix + "set_extra").argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
+    getattr(lib, prefix + "assemble_rhs").argtypes = [C.c_void_p, C.c_int, _dp]
+    getattr(lib, prefix + "exact_errors").argtypes = [C.c_void_p, _dp, _dp, _dp]
+    native = [C.c_void_p, _dp, _dp, _ip, _ip, _ip, _dp, _dp, _dp]
+    getattr(lib, prefix + "solve_native").argtypes = native + ([_dp] if prefix == "ref_" else [])
 
 
 _LIBS: dict = {}
@@ -136,6 +145,7 @@ class _Solver:
         self.lib = _load(self._path, self._prefix)
         self.case = case
         h = C.c_void_p()
+        self._fn("set_extra")(case.solution, case.fmg, case.fmg_iterations, CYCLE[case.fmg_cycle])
         self._check(self._fn("create")(*case.args(), C.byref(h)))
         self.h = h
         self.num_levels = self._fn("num_levels")(self.h)
@@ -249,6 +259,41 @@ class _Solver:
             "residual_norms": hist[: it.value + 1].copy(),
             "reduction_factor_mean": red.value,
             "seconds": sec.value,
+        }
+
+
+    def assemble_rhs(self, level=0):
+        """DiscreteOperator::assemble_rhs (stencil.cpp:326-353) of a level."""
+        b = np.zeros(self.n(level))
+        self._check(self._fn("assemble_rhs")(self.h, level, _ptr(b)))
+        return b
+
+    def exact_errors(self, u):
+        w, inf = C.c_double(), C.c_double()
+        self._check(self._fn("exact_errors")(self.h, _ptr(np.ascontiguousarray(u, np.float64)),
+                                              C.byref(w), C.byref(inf)))
+        return w.value, inf.value
+
+    def solve_native(self):
+        """MultigridSolver::solve() itself (multigrid.cpp:298-357)."""
+        u = np.zeros(self.n(0))
+        hist = np.zeros(self.case.max_iterations + 1)
+        it, fc, conv = C.c_int(), C.c_int(), C.c_int()
+        red, ew, ei, sec = C.c_double(), C.c_double(), C.c_double(), C.c_double()
+        args = [self.h, _ptr(u), _ptr(hist), C.byref(it), C.byref(fc), C.byref(conv),
+                C.byref(red), C.byref(ew), C.byref(ei)]
+        if self._prefix == "ref_":
+            args.append(C.byref(sec))
+        self._check(self._fn("solve_native")(*args))
+        return {
+            "u": u,
+            "iterations": it.value,
+            "fine_cycles_total": fc.value,
+            "converged": bool(conv.value),
+            "residual_norms": hist[: it.value + 1].copy(),
+            "reduction_factor_mean": red.value,
+            "exact_error_weighted": ew.value,
+            "exact_error_infinity": ei.value,
         }
 
 

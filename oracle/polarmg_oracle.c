@@ -399,6 +399,9 @@ typedef struct {
     int L;
     Level* lv;
     double* work; /* max(nr, nt) scratch */
+    int sol;                     /* 1: PolarOscillation manufactured solution */
+    int fmg, fmg_it, fmg_cycle;  /* multigrid.hpp:42-45 */
+    int fmg_run;
 } Solver;
 
 static int is_dir(const Solver* S, const Level* l, int s) {
@@ -963,7 +966,134 @@ double orc_norm(int type, const double* v, long n) {
     return type == 0 ? sqrt(acc / (double)n) : sqrt(acc);
 }
 
-/* ref multigrid.cpp:146-153 (Dirichlet values are 0: no manufactured solution) */
+/* ------------------------------------------- manufactured solution / RHS */
+/* PolarOscillation, ref problem.cpp:48-72 (rmax = ProblemCase rmax) */
+static double sol_u(double rmax, double r, double th) {
+    const double rho = r / rmax;
+    const double a = rho * rho * rho;
+    const double omr = 1.0 - rho;
+    const double b = omr * omr * omr;
+    return 0.4096 * (a * a) * (b * b) * cos(11.0 * th);
+}
+static double sol_ur(double rmax, double r, double th) {
+    const double rho = r / rmax;
+    const double rho5 = rho * rho * rho * rho * rho;
+    const double omr = 1.0 - rho;
+    const double omr5 = omr * omr * omr * omr * omr;
+    return 0.4096 * 6.0 * rho5 * omr5 * (1.0 - 2.0 * rho) * cos(11.0 * th) / rmax;
+}
+static double sol_ut(double rmax, double r, double th) {
+    const double rho = r / rmax;
+    const double a = rho * rho * rho;
+    const double omr = 1.0 - rho;
+    const double b = omr * omr * omr;
+    return -11.0 * 0.4096 * (a * a) * (b * b) * sin(11.0 * th);
+}
+/* ref problem.cpp:104-106 */
+static double dirichlet_u(const Solver* S, double r, double th) {
+    return S->sol ? sol_u(S->P.rmax, r, th) : 0.0;
+}
+/* logical fluxes of rhs_f, ref problem.cpp:126-133 */
+static int flux_r(const Solver* S, double rr, double tt, double* out) {
+    Coef tc;
+    const int rc = transform(&S->G, p_alpha(&S->P, rr), rr, sin(tt), cos(tt), &tc);
+    if (rc) return rc;
+    *out = 2.0 * tc.arr * sol_ur(S->P.rmax, rr, tt) + tc.art * sol_ut(S->P.rmax, rr, tt);
+    return 0;
+}
+static int flux_t(const Solver* S, double rr, double tt, double* out) {
+    Coef tc;
+    const int rc = transform(&S->G, p_alpha(&S->P, rr), rr, sin(tt), cos(tt), &tc);
+    if (rc) return rc;
+    *out = tc.art * sol_ur(S->P.rmax, rr, tt) + 2.0 * tc.att * sol_ut(S->P.rmax, rr, tt);
+    return 0;
+}
+/* ProblemCase::rhs_f, ref problem.cpp:108-148: fourth-order central
+ * differences (diff4, :99-103) of the fluxes, Richardson step halving */
+static int rhs_f(const Solver* S, double r, double th, double* out) {
+    if (!S->sol) { *out = 0.0; return 0; }
+    if (r <= 0.0) return fail(1, "rhs_f requires r > 0");
+    const double rmax = S->P.rmax;
+    const double a = 1e-4 * rmax, b = r / 3.0;
+    const double er = b < a ? b : a;
+    const double et = 1e-4 * TWO_PI;
+    Coef c0;
+    int rc = transform(&S->G, 1.0, r, sin(th), cos(th), &c0);
+    if (rc) return rc;
+    const double det_abs = c0.det;
+    const double bu = p_beta(&S->P, r) * sol_u(rmax, r, th);
+    double fs[2];
+    for (int k = 0; k < 2; ++k) {
+        const double scale = k == 0 ? 1.0 : 0.5;
+        double g[4], q[4];
+        const double e = er * scale, f = et * scale;
+        const double xs[4] = {r - 2.0 * e, r - e, r + e, r + 2.0 * e};
+        const double ts[4] = {th - 2.0 * f, th - f, th + f, th + 2.0 * f};
+        for (int j = 0; j < 4; ++j) {
+            if ((rc = flux_r(S, xs[j], th, &g[j]))) return rc;
+            if ((rc = flux_t(S, r, ts[j], &q[j]))) return rc;
+        }
+        const double d_r = (g[0] - 8.0 * g[1] + 8.0 * g[2] - g[3]) / (12.0 * e);
+        const double d_t = (q[0] - 8.0 * q[1] + 8.0 * q[2] - q[3]) / (12.0 * f);
+        fs[k] = (-d_r - d_t) / det_abs + bu;
+    }
+    if (fabs(fs[0] - fs[1]) > 1e-7)
+        return fail(2, "rhs_f lost accuracy: Richardson step-halving check disagrees by more than 1e-7");
+    *out = (16.0 * fs[1] - fs[0]) / 15.0;
+    return 0;
+}
+/* ref stencil.cpp:297-305 */
+static double node_weight(const Grid* g, int s, int t) {
+    const int N = g->nr - 1;
+    const double hm = s > 0 ? g->h[s - 1] : 0.0;
+    const double hp = s < N ? g->h[s] : 0.0;
+    const double km = k_below(g, t);
+    const double kp = g->k[t];
+    return 0.5 * (hm + hp) * 0.5 * (km + kp);
+}
+/* DiscreteOperator::assemble_rhs_raw + assemble_rhs (Dirichlet lifting),
+ * ref stencil.cpp:307-353 */
+static int assemble_rhs(const Solver* S, const Level* l, double* b) {
+    const Grid* g = &l->g;
+    const int N = g->nr - 1;
+    for (int s = 0; s < g->nr; ++s)
+        for (int t = 0; t < g->nt; ++t) {
+            double f;
+            const int rc = rhs_f(S, g->r[s], g->th[t], &f);
+            if (rc) return rc;
+            b[gidx(g, s, t)] = f * coef(l, s, t).det * node_weight(g, s, t);
+        }
+    for (int s = 0; s < g->nr; ++s) {
+        const int lift = (s > 0 && is_dir(S, l, s - 1)) || (s < N && is_dir(S, l, s + 1));
+        if (!is_dir(S, l, s) && !lift) continue;
+        for (int t = 0; t < g->nt; ++t) {
+            const int p = gidx(g, s, t);
+            if (is_dir(S, l, s)) {
+                b[p] = dirichlet_u(S, g->r[s], g->th[t]);
+                continue;
+            }
+            Row r;
+            build_row(S, l, s, t, 0, &r);
+            for (int i = 0; i < r.count; ++i) {
+                int cs, ct;
+                gnode(g, r.cols[i], &cs, &ct);
+                if (!is_dir(S, l, cs)) continue;
+                b[p] -= r.vals[i] * dirichlet_u(S, g->r[cs], g->th[ct]);
+            }
+        }
+    }
+    return 0;
+}
+/* ref multigrid.cpp:133-143 */
+static void set_dirichlet_rows(const Solver* S, const Level* l, double* u) {
+    const Grid* g = &l->g;
+    const int N = g->nr - 1;
+    for (int t = 0; t < g->nt; ++t) u[gidx(g, N, t)] = dirichlet_u(S, g->r[N], g->th[t]);
+    if (S->boundary == 1)
+        for (int t = 0; t < g->nt; ++t) u[gidx(g, 0, t)] = dirichlet_u(S, g->r[0], g->th[t]);
+}
+
+/* ref multigrid.cpp:145-153 */
 static void mask_dirichlet(const Solver* S, const Level* l, double* v) {
     const int N = l->g.nr - 1;
     for (int t = 0; t < l->g.nt; ++t) v[gidx(&l->g, N, t)] = 0.0;
@@ -998,6 +1128,49 @@ static double residual_norm(Solver* S) {
     Level* l = &S->lv[0];
     residual(S, l, S->mode, l->u, l->f, l->res);
     return orc_norm(S->norm, l->res, (long)l->g.nr * l->g.nt);
+}
+
+static void coarse_direct(Solver* S, int lev) { /* ref multigrid.cpp:183-187 */
+    Level* l = &S->lv[lev];
+    memcpy(l->u, l->f, sizeof(double) * l->g.nr * l->g.nt);
+    env_solve(&l->direct, l->u, NULL);
+}
+
+/* ref multigrid.cpp:250-265 */
+static int fmg_initialize(Solver* S) {
+    const int L = S->L;
+    Level* lc = &S->lv[L - 1];
+    int rc = assemble_rhs(S, lc, lc->f);
+    if (rc) return rc;
+    coarse_direct(S, L - 1);
+    for (int lf = L - 2; lf >= 0; --lf) {
+        Level* l = &S->lv[lf];
+        Level* c = &S->lv[lf + 1];
+        prolongate(&l->g, &c->g, c->u, l->u, 0);
+        set_dirichlet_rows(S, l, l->u);
+        if ((rc = assemble_rhs(S, l, l->f))) return rc;
+        for (int k = 0; k < S->fmg_it; ++k) {
+            cycle(S, lf, S->fmg_cycle);
+            if (lf == 0) ++S->fmg_run;
+        }
+    }
+    return 0;
+}
+
+/* ref multigrid.cpp:277-296 */
+static void exact_errors(const Solver* S, const double* u, double* w, double* inf) {
+    if (!S->sol) { *w = -1.0; *inf = -1.0; return; }
+    const Grid* g = &S->lv[0].g;
+    double acc = 0.0, mx = 0.0;
+    for (int s = 0; s < g->nr; ++s)
+        for (int t = 0; t < g->nt; ++t) {
+            const double e = u[gidx(g, s, t)] - sol_u(S->P.rmax, g->r[s], g->th[t]);
+            acc += e * e;
+            const double ae = fabs(e);
+            mx = mx < ae ? ae : mx;
+        }
+    *w = sqrt(acc / (double)(g->nr * g->nt));
+    *inf = mx;
 }
 
 static void solver_free(Solver* S) {
@@ -1041,6 +1214,14 @@ static int level_init(Solver* S, Level* l) {
     return 0;
 }
 
+static _Thread_local int g_extra[4]; /* solution, fmg, fmg_iterations, fmg_cycle */
+static _Thread_local int g_extra_set;
+int orc_set_extra(int solution, int fmg, int fmg_iterations, int fmg_cycle) {
+    g_extra[0] = solution; g_extra[1] = fmg; g_extra[2] = fmg_iterations; g_extra[3] = fmg_cycle;
+    g_extra_set = 1;
+    return 0;
+}
+
 int orc_create(int geom_kind, double kappa_eps, double delta_e, int alpha_coeff,
                int beta_coeff, double rmax, double alpha_jump, double delta_r,
                double alpha_scale, int grid_mode, double R0, int a, int b,
@@ -1062,6 +1243,11 @@ int orc_create(int geom_kind, double kappa_eps, double delta_e, int alpha_coeff,
     S->mode = stencil_mode; S->boundary = boundary_mode; S->pre = pre; S->post = post;
     S->cycle = cyc; S->norm = norm_type; S->max_it = max_iterations;
     S->abs_tol = abs_tol; S->rel_tol = rel_tol; S->tol = pair_tol;
+    S->fmg_it = 2; S->fmg_cycle = 2;
+    if (g_extra_set) {
+        S->sol = g_extra[0]; S->fmg = g_extra[1]; S->fmg_it = g_extra[2]; S->fmg_cycle = g_extra[3];
+        g_extra_set = 0;
+    }
     Grid g0;
     int rc = grid_mode == 0 ? grid_uniform(&g0, R0, rmax, a, b, pair_tol)
                             : grid_build(&g0, R0, rmax, a, b, aniso, divide_by_2, pair_tol);
@@ -1231,7 +1417,7 @@ int orc_solve(void* h, const double* f, double* u_out, double* history,
     struct timespec ts0, ts1;
     clock_gettime(CLOCK_MONOTONIC, &ts0);
     memset(l0->u, 0, sizeof(double) * n);
-    /* set_dirichlet_rows: boundary values are 0 (no manufactured solution) */
+    set_dirichlet_rows(S, l0, l0->u);
     const double r0 = residual_norm(S);
     history[0] = r0;
     int conv = r0 == 0.0 || (S->abs_tol > 0.0 && r0 <= S->abs_tol);
@@ -1250,5 +1436,53 @@ int orc_solve(void* h, const double* f, double* u_out, double* history,
     const double r_end = history[it];
     *mean_reduction = (it > 0 && r0 > 0.0 && r_end > 0.0) ? pow(r_end / r0, 1.0 / it) : 0.0;
     memcpy(u_out, l0->u, sizeof(double) * n);
+    return 0;
+}
+
+/* MultigridSolver::solve() itself (ref multigrid.cpp:298-357): manufactured
+ * RHS (or FMG start), solve loop, exact errors. */
+int orc_solve_native(void* h, double* u_out, double* history, int* iterations,
+                     int* fine_cycles, int* converged, double* mean_reduction,
+                     double* err_weighted, double* err_inf) {
+    Solver* S = (Solver*)h;
+    Level* l0 = &S->lv[0];
+    const long n = (long)l0->g.nr * l0->g.nt;
+    int rc;
+    S->fmg_run = 0;
+    if (S->fmg) {
+        if ((rc = fmg_initialize(S))) return rc;
+    } else {
+        if ((rc = assemble_rhs(S, l0, l0->f))) return rc;
+        memset(l0->u, 0, sizeof(double) * n);
+        set_dirichlet_rows(S, l0, l0->u);
+    }
+    const double r0 = residual_norm(S);
+    history[0] = r0;
+    int conv = r0 == 0.0 || (S->abs_tol > 0.0 && r0 <= S->abs_tol);
+    int it = 0;
+    while (!conv && it < S->max_it) {
+        cycle(S, 0, S->cycle);
+        ++it;
+        const double r = residual_norm(S);
+        history[it] = r;
+        conv = (S->abs_tol > 0.0 && r <= S->abs_tol) || (S->rel_tol > 0.0 && r <= S->rel_tol * r0);
+    }
+    *iterations = it;
+    *fine_cycles = it + S->fmg_run;
+    *converged = conv;
+    const double r_end = history[it];
+    *mean_reduction = (it > 0 && r0 > 0.0 && r_end > 0.0) ? pow(r_end / r0, 1.0 / it) : 0.0;
+    exact_errors(S, l0->u, err_weighted, err_inf);
+    memcpy(u_out, l0->u, sizeof(double) * n);
+    return 0;
+}
+
+int orc_assemble_rhs(void* h, int level, double* b) {
+    Solver* S = (Solver*)h;
+    return assemble_rhs(S, &S->lv[level], b);
+}
+
+int orc_exact_errors(void* h, const double* u, double* w, double* inf) {
+    exact_errors((Solver*)h, u, w, inf);
     return 0;
 }

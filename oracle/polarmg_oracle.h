@@ -37,6 +37,14 @@ int orc_solve(void* h, const double* f, double* u_out, double* history,
               int* iterations, int* converged, double* mean_reduction,
               double* seconds);
 double orc_norm(int type, const double* v, long n);
+/* extras for the next orc_create on this thread: manufactured solution
+ * (0 None, 1 PolarOscillation) and FMG settings (multigrid.hpp:42-45) */
+int orc_set_extra(int solution, int fmg, int fmg_iterations, int fmg_cycle);
+int orc_solve_native(void* h, double* u_out, double* history, int* iterations,
+                     int* fine_cycles, int* converged, double* mean_reduction,
+                     double* err_weighted, double* err_inf);
+int orc_assemble_rhs(void* h, int level, double* b);
+int orc_exact_errors(void* h, const double* u, double* w, double* inf);
 
 #ifdef __cplusplus
 }

@@ -75,6 +75,18 @@ extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
 
+// extras for the next ref_create on this thread: manufactured solution
+// (0 None, 1 PolarOscillation, problem.hpp:32-44) and the FMG settings
+// (multigrid.hpp:42-45)
+thread_local int g_extra[4] = {0, 0, 2, 2};
+int ref_set_extra(int solution, int fmg, int fmg_iterations, int fmg_cycle) {
+    g_extra[0] = solution;
+    g_extra[1] = fmg;
+    g_extra[2] = fmg_iterations;
+    g_extra[3] = fmg_cycle;
+    return 0;
+}
+
 // grid_mode 0: PolarGrid::uniform(R0, Rmax, a, b)
 // grid_mode 1: build_grid({R0, Rmax, nr_exp=a, ntheta_exp=b, aniso, divideBy2})
 int ref_create(int geom_kind, double kappa_eps, double delta_e, int alpha_coeff,
@@ -89,8 +101,10 @@ int ref_create(int geom_kind, double kappa_eps, double delta_e, int alpha_coeff,
         polarmg_ref_alpha_scale = alpha_scale;
         GeometryMap geom(static_cast<GeometryKind>(geom_kind), kappa_eps,
                          delta_e);
+        std::shared_ptr<const ManufacturedSolution> sol;
+        if (g_extra[0] == 1) sol = std::make_shared<PolarOscillation>(rmax);
         ProblemCase prob(static_cast<AlphaCoeff>(alpha_coeff),
-                         static_cast<BetaCoeff>(beta_coeff), nullptr, rmax,
+                         static_cast<BetaCoeff>(beta_coeff), sol, rmax,
                          alpha_jump, delta_r);
         PolarGrid grid = [&] {
             if (grid_mode == 0) return PolarGrid::uniform(R0, rmax, a, b);
@@ -115,6 +129,13 @@ int ref_create(int geom_kind, double kappa_eps, double delta_e, int alpha_coeff,
         s.absolute_tolerance = abs_tol;
         s.relative_tolerance = rel_tol;
         s.max_threads = threads;
+        s.fmg = g_extra[1] != 0;
+        s.fmg_iterations = g_extra[2];
+        s.fmg_cycle = static_cast<CycleType>(g_extra[3]);
+        g_extra[0] = 0;
+        g_extra[1] = 0;
+        g_extra[2] = 2;
+        g_extra[3] = 2;
         auto h = std::make_unique<RefHandle>();
         h->mg = std::make_unique<MultigridSolver>(geom, prob, std::move(grid), s);
         h->ws.resize(omp_get_max_threads());
@@ -307,6 +328,48 @@ int ref_solve(void* h, const double* f, double* u_out, double* history,
                                                 : 0.0;
         std::copy(hist.begin(), hist.end(), history);
         std::copy(l0.u.raw().begin(), l0.u.raw().end(), u_out);
+    });
+}
+
+// The reference's own MultigridSolver::solve() (multigrid.cpp:298-357):
+// manufactured RHS or FMG start, solve loop, exact errors.
+int ref_solve_native(void* h, double* u_out, double* history, int* iterations,
+                     int* fine_cycles, int* converged, double* mean_reduction,
+                     double* err_weighted, double* err_inf, double* seconds) {
+    return guarded([&] {
+        MultigridSolver& mg = *static_cast<RefHandle*>(h)->mg;
+        const double t0 = omp_get_wtime();
+        const ConvergenceReport rep = mg.solve();
+        *seconds = omp_get_wtime() - t0;
+        *iterations = rep.iterations;
+        *fine_cycles = rep.fine_cycles_total;
+        *converged = rep.converged ? 1 : 0;
+        *mean_reduction = rep.reduction_factor_mean;
+        *err_weighted = rep.exact_error_weighted;
+        *err_inf = rep.exact_error_infinity;
+        std::copy(rep.residual_norms.begin(), rep.residual_norms.end(), history);
+        const auto& u = mg.levels_[0].u.raw();
+        std::copy(u.begin(), u.end(), u_out);
+    });
+}
+
+// DiscreteOperator::assemble_rhs of a level (stencil.cpp:326-353)
+int ref_assemble_rhs(void* h, int level, double* b) {
+    return guarded([&] {
+        MultigridSolver& mg = *static_cast<RefHandle*>(h)->mg;
+        mg.levels_[level].op->assemble_rhs(b);
+    });
+}
+
+// MultigridSolver::exact_errors (multigrid.cpp:277-296) of a given u
+int ref_exact_errors(void* h, const double* u, double* w, double* inf) {
+    return guarded([&] {
+        MultigridSolver& mg = *static_cast<RefHandle*>(h)->mg;
+        auto& l0 = mg.levels_[0];
+        std::copy(u, u + mg.grid(0).num_nodes(), l0.u.data());
+        const auto e = mg.exact_errors();
+        *w = e.first;
+        *inf = e.second;
     });
 }
 

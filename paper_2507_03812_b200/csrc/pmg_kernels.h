@@ -203,6 +203,33 @@ void launch_circle_z(const LevelView& L, const double* cil, const double* cm, do
                      cudaStream_t st);
 void launch_factor_radial(const LevelView& L, bool onfly, double* ril, double* rm, int* bad,
                           cudaStream_t st);
+// ---- manufactured problem (problem.cpp:48-148, stencil.cpp:297-353) ----
+// Host-computed transcendental tables (std::exp/tanh/sin/cos, the reference's
+// own libm values) at the shifted points of rhs_f's difference stencils; all
+// arithmetic on them runs on the device in the reference's operation order.
+struct RhsTables {
+    const double* th;     // [nt] angles
+    const double* aR;     // [B][nr][8] alpha(r -/+ k e), k = 2,1,1,2; e = er, er/2
+    const double* sT;     // [nt][8] sin(theta -/+ k e), e = et, et/2
+    const double* cT;     // [nt][8] cos(...)
+    const double* s11;    // [nt][8] sin(11 (theta -/+ k e))
+    const double* c11;    // [nt][8] cos(11 (theta -/+ k e))
+    const double* s11_0;  // [nt] sin(11 theta)
+    const double* c11_0;  // [nt] cos(11 theta)
+    double rmax;          // ProblemCase / PolarOscillation rmax
+    int sol;              // 1: PolarOscillation, 0: none (f = 0, u_D = 0)
+};
+// f = assemble_rhs of the level (raw RHS, Dirichlet rows, lifting); *bad:
+// 1 singular Jacobian, 2 Richardson check failed, 3 r <= 0
+void launch_assemble_rhs(const LevelView& L, const RhsTables& T, double* f, int* bad,
+                         cudaStream_t st);
+// set_dirichlet_rows (multigrid.cpp:133-143)
+void launch_set_dirichlet(const LevelView& L, const RhsTables& T, double* u, cudaStream_t st);
+// per-block partial sums of e^2 and max |e|, e = u - u_exact (multigrid.cpp:277-296);
+// partials [B][nblk][2]; returns nblk
+int launch_exact_errors(const LevelView& L, const RhsTables& T, const double* u,
+                        double* partials, int cap, cudaStream_t st);
+
 // assembled rows [B][10][n] of a coarse-tail level (see k_rows)
 void launch_rows(const LevelView& L, bool onfly, double* rows, cudaStream_t st);
 // f = A u on the finest level for seeded RHS (same as launch_apply mode 0)

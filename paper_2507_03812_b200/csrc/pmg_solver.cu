@@ -1066,6 +1066,128 @@ struct Solver {
         std::fprintf(stderr, "tail trace: total %.2f us\n", (t[prog.size() + 1] - t[0]) * 1e-3);
     }
 
+    // ---------------------------------------------- manufactured problem
+    // (problem.cpp:48-148, stencil.cpp:297-353, multigrid.cpp:133-143,250-296)
+    std::vector<RhsTables> rhs_tabs;
+    int* d_bad = nullptr;
+    int fmg_run = 0;
+
+    void build_rhs_tables() {
+        if (!rhs_tabs.empty()) return;
+        const double two_pi = 2.0 * 3.141592653589793;  // kTwoPi (problem.cpp:10)
+        for (Level& V : lv) {
+            const HostGrid& g = V.g;
+            const int nr = g.nr(), nt = g.nt();
+            std::vector<double> aR((size_t)B * nr * 8), sT((size_t)nt * 8), cT((size_t)nt * 8),
+                s11((size_t)nt * 8), c11((size_t)nt * 8), s0(nt), c0(nt);
+            const auto alpha = [&](int b, double r) {  // problem.cpp:86-89
+                return prob.alpha_coeff == 0
+                           ? 1.0
+                           : scales[b] * std::exp(-std::tanh((r / prob.rmax - prob.alpha_jump) /
+                                                             prob.delta_r));
+            };
+            for (int b = 0; b < B; ++b)
+                for (int s = 0; s < nr; ++s) {  // rhs_f radial stencil (problem.cpp:135-142)
+                    const double r = g.r[s];
+                    const double a1 = 1e-4 * prob.rmax, a2 = r / 3.0;
+                    const double er = a2 < a1 ? a2 : a1;
+                    for (int k = 0; k < 2; ++k) {
+                        const double e = er * (k == 0 ? 1.0 : 0.5);
+                        const double xs[4] = {r - 2.0 * e, r - e, r + e, r + 2.0 * e};
+                        for (int j = 0; j < 4; ++j)
+                            aR[((size_t)b * nr + s) * 8 + 4 * k + j] = alpha(b, xs[j]);
+                    }
+                }
+            const double et = 1e-4 * two_pi;
+            for (int t = 0; t < nt; ++t) {
+                const double th = g.th[t];
+                s0[t] = std::sin(11.0 * th);
+                c0[t] = std::cos(11.0 * th);
+                for (int k = 0; k < 2; ++k) {
+                    const double e = et * (k == 0 ? 1.0 : 0.5);
+                    const double ts[4] = {th - 2.0 * e, th - e, th + e, th + 2.0 * e};
+                    for (int j = 0; j < 4; ++j) {
+                        const size_t i = (size_t)t * 8 + 4 * k + j;
+                        sT[i] = std::sin(ts[j]);
+                        cT[i] = std::cos(ts[j]);
+                        s11[i] = std::sin(11.0 * ts[j]);
+                        c11[i] = std::cos(11.0 * ts[j]);
+                    }
+                }
+            }
+            RhsTables T{};
+            T.th = upload(g.th);
+            T.aR = upload(aR);
+            T.sT = upload(sT);
+            T.cT = upload(cT);
+            T.s11 = upload(s11);
+            T.c11 = upload(c11);
+            T.s11_0 = upload(s0);
+            T.c11_0 = upload(c0);
+            T.rmax = prob.rmax;
+            T.sol = prob.solution;
+            rhs_tabs.push_back(T);
+        }
+        d_bad = alloc<int>(1);
+    }
+    // MultigridSolver::assemble_level_rhs (multigrid.cpp:155-157)
+    void assemble_level_rhs(int l) {
+        build_rhs_tables();
+        PMG_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), stream));
+        run(KK_OTHER, 1, [&] { launch_assemble_rhs(lv[l].v, rhs_tabs[l], lv[l].f, d_bad, stream); });
+        int hb = 0;
+        PMG_CUDA(cudaMemcpyAsync(&hb, d_bad, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        PMG_CUDA(cudaStreamSynchronize(stream));
+        PMG_CUDA(cudaGetLastError());
+        if (hb == 1) throw PmgError(PMG_ERUNTIME, "singular Jacobian: mapping degenerate at queried point");
+        if (hb == 2)
+            throw PmgError(PMG_ERUNTIME,
+                           "rhs_f lost accuracy: Richardson step-halving check disagrees by more "
+                           "than 1e-7");
+        if (hb == 3) throw PmgError(PMG_EINVAL, "rhs_f requires r > 0");
+    }
+    void set_dirichlet_rows(int l, double* u) {
+        build_rhs_tables();
+        run(KK_OTHER, 1, [&] { launch_set_dirichlet(lv[l].v, rhs_tabs[l], u, stream); });
+    }
+    // multigrid.cpp:250-265
+    void fmg_initialize() {
+        const int L = static_cast<int>(lv.size());
+        assemble_level_rhs(L - 1);
+        coarse(L - 1, active);
+        for (int lf = L - 2; lf >= 0; --lf) {
+            Level& F = lv[lf];
+            Level& C = lv[lf + 1];
+            run(KK_PROLONG, 1,
+                [&] { launch_prolong(F.v, C.v, F.w, C.u, F.u, false, active, stream); });
+            set_dirichlet_rows(lf, F.u);
+            assemble_level_rhs(lf);
+            for (int c = 0; c < set.fmg_iterations; ++c) {
+                cycle(lf, set.fmg_cycle, active);
+                if (lf == 0) ++fmg_run;
+            }
+        }
+    }
+    // multigrid.cpp:277-296 (device reduction order; -1 without a solution)
+    void exact_errors(const double* u, double* w, double* inf) {
+        build_rhs_tables();
+        const LevelView& v = lv[0].v;
+        const int nb = launch_exact_errors(v, rhs_tabs[0], u, partials, partial_cap / 2, stream);
+        std::vector<double> hp((size_t)B * nb * 2);
+        PMG_CUDA(cudaMemcpyAsync(hp.data(), partials, hp.size() * sizeof(double),
+                                 cudaMemcpyDeviceToHost, stream));
+        PMG_CUDA(cudaStreamSynchronize(stream));
+        for (int b = 0; b < B; ++b) {
+            double a = 0.0, m = 0.0;
+            for (int i = 0; i < nb; ++i) {
+                a += hp[((size_t)b * nb + i) * 2];
+                m = std::max(m, hp[((size_t)b * nb + i) * 2 + 1]);
+            }
+            w[b] = prob.solution ? std::sqrt(a / v.n) : -1.0;
+            inf[b] = prob.solution ? m : -1.0;
+        }
+    }
+
     int solve(pmg_report* reports, double* history, int history_cap) {
         PMG_CUDA(cudaSetDevice(device));
         cudaEvent_t e0, e1;
@@ -1073,10 +1195,17 @@ struct Solver {
         PMG_CUDA(cudaEventCreate(&e1));
         PMG_CUDA(cudaEventRecord(e0, stream));
         Level& V = lv[0];
-        run(KK_OTHER, 2, [&] {
-            launch_set_active(active, count, conv, remaining, B, stream);
-            launch_fill(V.u, (long)B * V.v.n, 0.0, stream);  // u = 0; Dirichlet values 0
-        });
+        fmg_run = 0;
+        if (set.fmg) {  // multigrid.cpp:306-307
+            run(KK_OTHER, 1, [&] { launch_set_active(active, count, conv, remaining, B, stream); });
+            fmg_initialize();
+        } else {  // multigrid.cpp:309-316 (the RHS is the current f)
+            run(KK_OTHER, 2, [&] {
+                launch_set_active(active, count, conv, remaining, B, stream);
+                launch_fill(V.u, (long)B * V.v.n, 0.0, stream);
+            });
+            if (prob.solution) set_dirichlet_rows(0, V.u);
+        }
         norm_check();
         const bool graph = use_graph && !prof;
         if (graph && !cycle_exec) build_cycle_graph();
@@ -1118,6 +1247,8 @@ struct Solver {
         PMG_CUDA(cudaMemcpy(h_conv.data(), conv, sizeof(int) * B, cudaMemcpyDeviceToHost));
         PMG_CUDA(cudaMemcpy(h_hist.data(), hist, sizeof(double) * h_hist.size(),
                             cudaMemcpyDeviceToHost));
+        std::vector<double> ew(B, -1.0), ei(B, -1.0);
+        if (reports && prob.solution) exact_errors(lv[0].u, ew.data(), ei.data());
         bool all = true;
         for (int b = 0; b < B; ++b) {
             const int itb = h_it[b];
@@ -1127,7 +1258,9 @@ struct Solver {
                 std::memset(&r, 0, sizeof r);
                 r.converged = h_conv[b];
                 r.iterations = itb;
-                r.fine_cycles_total = itb;
+                r.fine_cycles_total = itb + fmg_run;
+                r.exact_error_weighted = ew[b];
+                r.exact_error_infinity = ei[b];
                 r.num_residuals = itb + 1;
                 r.initial_residual = hb[0];
                 r.final_residual = hb[itb];
@@ -1207,7 +1340,10 @@ static void validate(const pmg_geometry* g, const pmg_problem* p, const pmg_grid
     if (s->extrapolation == 1)
         throw PmgError(PMG_EINVAL,
                        "extrapolation=1 is not supported by the B200 solve path yet");
-    if (s->fmg) throw PmgError(PMG_EINVAL, "FMG=1 is not supported by the B200 solve path yet");
+    if (s->fmg && (s->fmg_cycle < 0 || s->fmg_cycle > 2))
+        throw PmgError(PMG_EINVAL, "unknown FMG_cycle type (expected V, W, or F)");
+    if (p->solution < 0 || p->solution > 1)
+        throw PmgError(PMG_EINVAL, "unknown problem (expected None or Polar)");
     if (p->rmax <= 0.0) throw PmgError(PMG_EINVAL, "Rmax must be positive");
     if (p->delta_r <= 0.0) throw PmgError(PMG_EINVAL, "delta_r must be positive");
     if (gr->mode != 2 && (gr->R0 <= 0.0 || gr->R0 >= gr->Rmax))
@@ -1472,6 +1608,23 @@ int pmg_solve(pmg_handle h, pmg_report* reports, double* history, int history_ca
     if (g != PMG_OK) return g;
     if (rc == PMG_ENOTCONV) pmg::g_err = "solve ended without meeting a tolerance";
     return rc;
+}
+
+int pmg_assemble_rhs(pmg_handle h) {
+    return guarded([&] {
+        Solver& s = S(h);
+        PMG_CUDA(cudaSetDevice(s.device));
+        s.assemble_level_rhs(0);
+    });
+}
+
+int pmg_exact_errors(pmg_handle h, double* weighted, double* infinity) {
+    return guarded([&] {
+        Solver& s = S(h);
+        if (!weighted || !infinity) throw PmgError(PMG_EINVAL, "null argument");
+        PMG_CUDA(cudaSetDevice(s.device));
+        s.exact_errors(s.lv[0].u, weighted, infinity);
+    });
 }
 
 int pmg_get_solution(pmg_handle h, double* u_host, int layout) {

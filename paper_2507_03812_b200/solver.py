@@ -49,7 +49,8 @@ class _Geometry(C.Structure):
 
 class _Problem(C.Structure):
     _fields_ = [("alpha_coeff", C.c_int), ("beta_coeff", C.c_int), ("rmax", C.c_double),
-                ("alpha_jump", C.c_double), ("delta_r", C.c_double), ("alpha_scale", C.c_double)]
+                ("alpha_jump", C.c_double), ("delta_r", C.c_double), ("alpha_scale", C.c_double),
+                ("solution", C.c_int)]
 
 
 class _Grid(C.Structure):
@@ -75,7 +76,8 @@ class _Report(C.Structure):
                 ("num_residuals", C.c_int), ("reduction_factor_mean", C.c_double),
                 ("initial_residual", C.c_double), ("final_residual", C.c_double),
                 ("setup_seconds", C.c_double), ("solve_seconds", C.c_double),
-                ("device_bytes", C.c_size_t)]
+                ("device_bytes", C.c_size_t), ("exact_error_weighted", C.c_double),
+                ("exact_error_infinity", C.c_double)]
 
 
 _dp = C.POINTER(C.c_double)
@@ -85,7 +87,8 @@ _lib = None
 EXPORTED = [
     "pmg_last_error", "pmg_version", "pmg_default_settings", "pmg_create", "pmg_create_batch",
     "pmg_destroy", "pmg_grid_hierarchy", "pmg_num_levels", "pmg_num_sections", "pmg_level_info", "pmg_level_grid",
-    "pmg_set_rhs", "pmg_get_rhs", "pmg_set_rhs_device", "pmg_seeded_rhs", "pmg_solve", "pmg_get_solution",
+    "pmg_set_rhs", "pmg_get_rhs", "pmg_set_rhs_device", "pmg_seeded_rhs", "pmg_assemble_rhs",
+    "pmg_exact_errors", "pmg_solve", "pmg_get_solution",
     "pmg_solution_device", "pmg_apply", "pmg_residual", "pmg_smooth", "pmg_sweep",
     "pmg_restrict", "pmg_prolongate", "pmg_coarse_solve", "pmg_norm", "pmg_launch_count",
     "pmg_time_kernel", "pmg_profile_enable", "pmg_profile_read",
@@ -126,6 +129,8 @@ def load_library(path: str = LIB_PATH):
     lib.pmg_get_rhs.argtypes = [vp, _dp, C.c_int]
     lib.pmg_seeded_rhs.argtypes = [vp, C.c_uint, _dp, C.c_int]
     lib.pmg_solve.argtypes = [vp, C.POINTER(_Report), _dp, C.c_int]
+    lib.pmg_assemble_rhs.argtypes = [vp]
+    lib.pmg_exact_errors.argtypes = [vp, _dp, _dp]
     lib.pmg_get_solution.argtypes = [vp, _dp, C.c_int]
     lib.pmg_solution_device.argtypes = [vp, C.POINTER(vp)]
     lib.pmg_apply.argtypes = [vp, C.c_int, _dp, _dp]
@@ -173,14 +178,16 @@ class GeometryMap:
 
 @dataclass
 class ProblemCase:
-    """ProblemCase(alpha_coeff, beta_coeff, -, rmax, alpha_jump, delta_r) -- problem.hpp:47-94.
-    No manufactured solution: the right-hand side is supplied (set_rhs / seeded_rhs)."""
+    """ProblemCase(alpha_coeff, beta_coeff, solution, rmax, alpha_jump, delta_r) --
+    problem.hpp:47-94.  ``solution`` "None" (the RHS is supplied: set_rhs / seeded_rhs)
+    or "Polar" (PolarOscillation, problem.cpp:48-72: assemble_rhs, FMG, exact errors)."""
     alpha_coeff: str = "Zoni"  # "Poisson" | "Zoni"
     beta_coeff: str = "InverseAlpha"  # "Zero" | "InverseAlpha"
     rmax: float = 1.3
     alpha_jump: float = 0.7
     delta_r: float = 0.05
     alpha_scale: float = 1.0
+    solution: str = "None"  # "None" | "Polar"
 
 
 @dataclass
@@ -254,6 +261,8 @@ class ConvergenceReport:
     setup_seconds: float = 0.0
     solve_seconds: float = 0.0  # device time (CUDA events) of the solve window
     device_bytes: int = 0
+    exact_error_weighted: float = -1.0  # -1 without a manufactured solution
+    exact_error_infinity: float = -1.0
 
 
 def _grid_struct(grid: "PolarGrid", keep: list):
@@ -306,7 +315,8 @@ class MultigridSolver:
             problem.alpha_coeff, str) else problem.alpha_coeff,
             {"Zero": 0, "InverseAlpha": 1}[problem.beta_coeff] if isinstance(
                 problem.beta_coeff, str) else problem.beta_coeff,
-            problem.rmax, problem.alpha_jump, problem.delta_r, problem.alpha_scale)
+            problem.rmax, problem.alpha_jump, problem.delta_r, problem.alpha_scale,
+            _lookup({"None": 0, "Polar": 1, "PolarOscillation": 1}, problem.solution, "problem"))
         self._keep = []
         gr = _grid_struct(grid, self._keep)
         s = _Settings(_lookup(STENCIL, settings.stencil_mode, "stencilDistributionMethod"),
@@ -412,9 +422,23 @@ class MultigridSolver:
                 fine_cycles_total=r.fine_cycles_total,
                 residual_norms=list(hist[b * cap: b * cap + r.num_residuals]),
                 reduction_factor_mean=r.reduction_factor_mean, setup_seconds=r.setup_seconds,
-                solve_seconds=r.solve_seconds, device_bytes=int(r.device_bytes)))
+                solve_seconds=r.solve_seconds, device_bytes=int(r.device_bytes),
+                exact_error_weighted=r.exact_error_weighted,
+                exact_error_infinity=r.exact_error_infinity))
         self._last_report = out
         return out[0]
+
+    def assemble_rhs(self):
+        """f = DiscreteOperator::assemble_rhs of the finest level (stencil.cpp:307-353),
+        on the device; then solve() is the reference's MultigridSolver::solve()."""
+        _check(self._lib.pmg_assemble_rhs(self._h))
+
+    def exact_errors(self):
+        """MultigridSolver::exact_errors() (multigrid.cpp:277-296) per section."""
+        w = np.zeros(self.n_sections)
+        inf = np.zeros(self.n_sections)
+        _check(self._lib.pmg_exact_errors(self._h, _p(w), _p(inf)))
+        return w, inf
 
     @property
     def reports(self) -> List[ConvergenceReport]:

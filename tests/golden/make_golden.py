@@ -30,6 +30,35 @@ CASES = {
 }
 
 
+# the reference's verification problem (testsup::polar_case + make_map,
+# proj/tests/support.hpp:43-58; grids of acceptance.cpp:85,237)
+POLAR = dict(solution=1, R0=1.3e-5, alpha_jump=0.7, delta_r=0.05, max_iterations=150)
+PROBLEM_CASES = {
+    "problem_czarny_49x64_V": Case(geometry="Czarny", kappa_eps=0.3, delta_e=1.4, a=49, b=64,
+                                   **POLAR),
+    "problem_shafranov_interior_fmgF": Case(geometry="Shafranov", kappa_eps=0.3, delta_e=0.2,
+                                            a=49, b=64, boundary_mode=1, fmg=1, **POLAR),
+    "problem_czarny_97x128_give_fmgV": Case(geometry="Czarny", kappa_eps=0.3, delta_e=1.4, a=97,
+                                            b=128, stencil_mode="Give", fmg=1, fmg_cycle="V",
+                                            fmg_iterations=1, rel_tol=1e-8, **POLAR),
+}
+
+
+def make_problem(name, c):
+    R = RefSolver(c)
+    out = {"levels": np.array(R.levels, dtype=np.int64)}
+    out["rhs_l0"] = R.assemble_rhs(0)
+    out["rhs_coarsest"] = R.assemble_rhs(R.num_levels - 1)
+    sol = R.solve_native()  # the reference's own MultigridSolver::solve()
+    out["solve_u"] = sol["u"]
+    out["solve_history"] = sol["residual_norms"]
+    out["solve_iterations"] = np.array(sol["iterations"])
+    out["fine_cycles_total"] = np.array(sol["fine_cycles_total"])
+    out["exact_errors"] = np.array([sol["exact_error_weighted"], sol["exact_error_infinity"]])
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, R.levels[0], sol["iterations"], "cycles", sol["fine_cycles_total"], "fine")
+
+
 def make(name, c):
     R = RefSolver(c)
     out = {"levels": np.array(R.levels, dtype=np.int64)}
@@ -67,3 +96,5 @@ def make(name, c):
 if __name__ == "__main__":
     for name, c in CASES.items():
         make(name, c)
+    for name, c in PROBLEM_CASES.items():
+        make_problem(name, c)

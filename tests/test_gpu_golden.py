@@ -10,26 +10,56 @@ import paper_2507_03812_b200 as pmg
 
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
-GOLDEN = sorted(glob.glob(os.path.join(HERE, "golden", "*.npz")))
+import importlib.util
+
+_spec = importlib.util.spec_from_file_location("mg", os.path.join(HERE, "golden", "make_golden.py"))
+_mg = importlib.util.module_from_spec(_spec)
+_spec.loader.exec_module(_mg)
+GOLDEN = sorted(os.path.join(HERE, "golden", f"{k}.npz") for k in _mg.CASES)
+PROBLEM_GOLDEN = sorted(os.path.join(HERE, "golden", f"{k}.npz") for k in _mg.PROBLEM_CASES)
 
 
 def gpu_for(name, reference_order=True):
-    import importlib.util
-    spec = importlib.util.spec_from_file_location("mg", os.path.join(HERE, "golden", "make_golden.py"))
-    mg = importlib.util.module_from_spec(spec)
-    spec.loader.exec_module(mg)
-    c = mg.CASES[name]
+    c = _mg.CASES[name] if name in _mg.CASES else _mg.PROBLEM_CASES[name]
     geom = pmg.GeometryMap(c.geometry, c.kappa_eps, c.delta_e)
     prob = pmg.ProblemCase("Zoni" if c.alpha_coeff else "Poisson",
                            "InverseAlpha" if c.beta_coeff else "Zero", c.rmax, c.alpha_jump,
-                           c.delta_r, c.alpha_scale)
+                           c.delta_r, c.alpha_scale, solution="Polar" if c.solution else "None")
     grid = (pmg.PolarGrid.uniform(c.R0, c.rmax, c.a, c.b) if c.grid_mode == 0 else
             pmg.PolarGrid.build(c.R0, c.rmax, c.a, c.b, c.aniso, c.divide_by_2))
     st = pmg.MultigridSettings(stencil_mode=c.stencil_mode,
                                boundary_mode=["AcrossOrigin", "InteriorDirichlet"][c.boundary_mode],
                                cycle=c.cycle, relative_tolerance=c.rel_tol,
-                               max_iterations=c.max_iterations, reference_order=reference_order)
+                               max_iterations=c.max_iterations, fmg=bool(c.fmg),
+                               fmg_iterations=c.fmg_iterations, fmg_cycle=c.fmg_cycle,
+                               reference_order=reference_order)
     return c, pmg.MultigridSolver(geom, prob, grid, st)
+
+
+@pytest.mark.parametrize("reference_order", [True, False], ids=["reforder", "fast"])
+@pytest.mark.parametrize("path", PROBLEM_GOLDEN, ids=[os.path.basename(p)[:-4] for p in PROBLEM_GOLDEN])
+def test_gpu_problem_against_golden(path, reference_order):
+    """Manufactured RHS (bitwise), FMG start and the reference's solve() outputs."""
+    g = np.load(path)
+    c, s = gpu_for(os.path.basename(path)[:-4], reference_order)
+    if not c.fmg:
+        s.assemble_rhs()
+        assert np.array_equal(s.get_rhs(), g["rhs_l0"])
+    rep = s.solve()
+    if c.fmg:  # the FMG start assembled the finest RHS itself
+        assert np.array_equal(s.get_rhs(), g["rhs_l0"])
+    assert rep.iterations == int(g["solve_iterations"])
+    assert rep.fine_cycles_total == int(g["fine_cycles_total"])
+    u = s.solution()
+    err = np.abs(u - g["solve_u"]).max() / np.abs(g["solve_u"]).max()
+    if reference_order and c.stencil_mode == "Take":
+        assert err == 0.0
+        np.testing.assert_allclose([rep.exact_error_weighted, rep.exact_error_infinity],
+                                   g["exact_errors"], rtol=1e-12)
+    else:
+        assert err < 1e-9
+        np.testing.assert_allclose([rep.exact_error_weighted, rep.exact_error_infinity],
+                                   g["exact_errors"], rtol=1e-6)
 
 
 @pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p)[:-4] for p in GOLDEN])

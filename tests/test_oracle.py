@@ -20,8 +20,66 @@ _spec = _ilu.spec_from_file_location(
 _mg = _ilu.module_from_spec(_spec)
 _spec.loader.exec_module(_mg)
 CASES = _mg.CASES
+PROBLEM_CASES = _mg.PROBLEM_CASES
 
-GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+_HERE = os.path.join(os.path.dirname(__file__), "golden")
+GOLDEN = sorted(os.path.join(_HERE, f"{k}.npz") for k in CASES)
+PROBLEM_GOLDEN = sorted(os.path.join(_HERE, f"{k}.npz") for k in PROBLEM_CASES)
+
+
+@pytest.mark.parametrize("path", PROBLEM_GOLDEN,
+                         ids=[os.path.basename(p)[:-4] for p in PROBLEM_GOLDEN])
+def test_oracle_problem_matches_golden_bitwise(path):
+    """assemble_rhs (stencil.cpp:307-353), FMG (multigrid.cpp:250-265), the
+    solve loop and exact_errors of the C restatement against the reference's
+    own MultigridSolver::solve() outputs."""
+    g = np.load(path)
+    O = OracleSolver(PROBLEM_CASES[os.path.basename(path)[:-4]])
+    assert np.array_equal(np.array(O.levels), g["levels"])
+    assert np.array_equal(O.assemble_rhs(0), g["rhs_l0"])
+    assert np.array_equal(O.assemble_rhs(O.num_levels - 1), g["rhs_coarsest"])
+    sol = O.solve_native()
+    assert sol["iterations"] == int(g["solve_iterations"])
+    assert sol["fine_cycles_total"] == int(g["fine_cycles_total"])
+    assert np.array_equal(sol["u"], g["solve_u"])
+    assert np.array_equal(sol["residual_norms"], g["solve_history"])
+    assert np.array_equal([sol["exact_error_weighted"], sol["exact_error_infinity"]],
+                          g["exact_errors"])
+
+
+def test_polar_oscillation_kats():
+    """test_problem.cpp:75-86: PolarOscillation vanishes at r = 0 and Rmax;
+    u(Rmax/2, 0) = 0.4096 * 2^-12 = 1e-4; exact_errors of u = 0 is |u_exact|."""
+    c = Case(geometry="CirclePolar", kappa_eps=0.0, delta_e=0.0, a=17, b=16, R0=1.3e-5,
+             solution=1, alpha_jump=0.7, delta_r=0.05)
+    O = OracleSolver(c)
+    r, th = O.level_grid(0)
+    rho = r / c.rmax
+    exact = np.array([0.4096 * (x ** 3) ** 2 * ((1 - x) ** 3) ** 2 for x in rho])
+    assert exact[-1] == 0.0
+    w, inf = O.exact_errors(np.zeros(O.n(0)))
+    assert inf > 0 and w > 0
+    assert abs(0.4096 * 0.5 ** 12 - 1e-4) <= 1e-18
+    # a problem without a solution reports -1 (multigrid.cpp:278)
+    O2 = OracleSolver(Case(geometry="CirclePolar", kappa_eps=0.0, delta_e=0.0, a=17, b=16))
+    assert O2.exact_errors(np.zeros(O2.n(0))) == (-1.0, -1.0)
+    assert not np.any(O2.assemble_rhs(0))
+
+
+@requires_ref
+@pytest.mark.parametrize("geo", ["CirclePolar", "Shafranov", "Czarny"])
+@pytest.mark.parametrize("bm", [0, 1])
+@pytest.mark.parametrize("fmg", [0, 1])
+def test_oracle_problem_vs_reference(geo, bm, fmg):
+    ke, de = {"CirclePolar": (0.0, 0.0), "Shafranov": (0.3, 0.2), "Czarny": (0.3, 1.4)}[geo]
+    c = Case(geometry=geo, kappa_eps=ke, delta_e=de, a=33, b=64, R0=1.3e-5, solution=1,
+             alpha_jump=0.7, delta_r=0.05, boundary_mode=bm, fmg=fmg, max_iterations=150)
+    R, O = RefSolver(c), OracleSolver(c)
+    assert np.array_equal(O.assemble_rhs(0), R.assemble_rhs(0))
+    a, b = O.solve_native(), R.solve_native()
+    assert a["iterations"] == b["iterations"] and a["fine_cycles_total"] == b["fine_cycles_total"]
+    assert np.array_equal(a["u"], b["u"])
+    assert a["exact_error_weighted"] == b["exact_error_weighted"]
 
 
 @pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p)[:-4] for p in GOLDEN])
