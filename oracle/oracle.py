@@ -74,6 +74,7 @@ class Case:
     fmg: int = 0
     fmg_iterations: int = 2
     fmg_cycle: str = "F"
+    extrapolation: int = 0
     extra: dict = field(default_factory=dict)
 
     def args(self):
@@ -114,7 +115,7 @@ def _bind(lib, prefix):
     getattr(lib, prefix + "solve").argtypes = [C.c_void_p, _dp, _dp, _dp, _ip, _ip, _dp, _dp]
     getattr(lib, prefix + "row").argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, _ip, _dp, _ip]
     getattr(lib, prefix + "level_coeffs").argtypes = [C.c_void_p, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp]
-    getattr(lib, prefix + "set_extra").argtypes = [C.c_int, C.c_int, C.c_int, C.c_int]
+    getattr(lib, prefix + "set_extra").argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]
     getattr(lib, prefix + "assemble_rhs").argtypes = [C.c_void_p, C.c_int, _dp]
     getattr(lib, prefix + "exact_errors").argtypes = [C.c_void_p, _dp, _dp, _dp]
     native = [C.c_void_p, _dp, _dp, _ip, _ip, _ip, _dp, _dp, _dp]
@@ -145,7 +146,8 @@ class _Solver:
         self.lib = _load(self._path, self._prefix)
         self.case = case
         h = C.c_void_p()
-        self._fn("set_extra")(case.solution, case.fmg, case.fmg_iterations, CYCLE[case.fmg_cycle])
+        self._fn("set_extra")(case.solution, case.fmg, case.fmg_iterations, CYCLE[case.fmg_cycle],
+                              case.extrapolation)
         self._check(self._fn("create")(*case.args(), C.byref(h)))
         self.h = h
         self.num_levels = self._fn("num_levels")(self.h)

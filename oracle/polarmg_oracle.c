@@ -401,6 +401,7 @@ typedef struct {
     double* work; /* max(nr, nt) scratch */
     int sol;                     /* 1: PolarOscillation manufactured solution */
     int fmg, fmg_it, fmg_cycle;  /* multigrid.hpp:42-45 */
+    int ex;                      /* implicit extrapolation (multigrid.hpp:41) */
     int fmg_run;
 } Solver;
 
@@ -692,14 +693,14 @@ static int smoother_init(const Solver* S, Level* l) {
 }
 
 /* ref smoother.cpp:162-182 */
-static void take_rhs_circle(const Solver* S, const Level* l, int s, double* u, const double* f) {
+static void take_rhs_circle(const Solver* S, const Level* l, int s, double* u, const double* f, int ex) {
     const int nt = l->g.nt, base = s * nt;
     if (is_dir(S, l, s)) { for (int t = 0; t < nt; ++t) u[base + t] = f[base + t]; return; }
     Row r;
     for (int t = 0; t < nt; ++t) {
         const int p = base + t;
         build_row(S, l, s, t, 1, &r);
-        double acc = f[p];
+        double acc = ex ? 0.75 * f[p] : f[p];
         for (int i = 0; i < r.count; ++i) {
             const int c = r.cols[i];
             if (c >= base && c < base + nt) continue;
@@ -710,14 +711,14 @@ static void take_rhs_circle(const Solver* S, const Level* l, int s, double* u, c
 }
 
 /* ref smoother.cpp:184-205 */
-static void take_rhs_radial(const Solver* S, const Level* l, int t, double* u, const double* f) {
+static void take_rhs_radial(const Solver* S, const Level* l, int t, double* u, const double* f, int ex) {
     const int split = l->g.split, len = l->g.nr - split, base = split * l->g.nt + t * len;
     Row r;
     for (int i = 0; i < len; ++i) {
         const int s = split + i, p = base + i;
         if (is_dir(S, l, s)) { u[p] = f[p]; continue; }
         build_row(S, l, s, t, 1, &r);
-        double acc = f[p];
+        double acc = ex ? 0.75 * f[p] : f[p];
         for (int e = 0; e < r.count; ++e) {
             const int c = r.cols[e];
             if (c >= base && c < base + len) continue;
@@ -863,29 +864,124 @@ static void give_rhs_radial(const Solver* S, const Level* l, int parity, double*
 }
 
 /* ref smoother.cpp:95-152 */
-static void sweep_circle(const Solver* S, const Level* l, int parity, double* u, const double* f, double* w) {
-    const int take = S->mode == 0;
+static void sweep_circle_x(const Solver* S, const Level* l, int parity, double* u, const double* f, double* w, int ex) {
+    const int take = ex || S->mode == 0;
     if (!take) give_rhs_circle(S, l, parity, u, f);
     const int split = l->g.split, nt = l->g.nt;
     const int lines = split > parity ? (split - parity + 1) / 2 : 0;
     for (int i = 0; i < lines; ++i) {
         const int s = parity + 2 * i;
-        if (take) take_rhs_circle(S, l, s, u, f);
+        if (take) take_rhs_circle(S, l, s, u, f, ex);
         if (s == 0 && S->boundary == 0) env_solve(&l->origin, u, w);
         else cyc_solve(nt, l->cl[s], l->cm[s], l->cc[s], u + s * nt, w);
     }
 }
 
-static void sweep_radial(const Solver* S, const Level* l, int parity, double* u, const double* f) {
-    const int take = S->mode == 0;
+static void sweep_radial_x(const Solver* S, const Level* l, int parity, double* u, const double* f, int ex) {
+    const int take = ex || S->mode == 0;
     if (!take) give_rhs_radial(S, l, parity, u, f);
     const int nt = l->g.nt, split = l->g.split, len = l->g.nr - split;
     const int lines = (nt - parity + 1) / 2;
     for (int i = 0; i < lines; ++i) {
         const int t = parity + 2 * i;
-        if (take) take_rhs_radial(S, l, t, u, f);
+        if (take) take_rhs_radial(S, l, t, u, f, ex);
         tri_solve(len, l->rl[t], l->rm[t], u + split * nt + t * len);
     }
+}
+
+static void sweep_circle(const Solver* S, const Level* l, int parity, double* u, const double* f, double* w) {
+    sweep_circle_x(S, l, parity, u, f, w, 0);
+}
+static void sweep_radial(const Solver* S, const Level* l, int parity, double* u, const double* f) {
+    sweep_radial_x(S, l, parity, u, f, 0);
+}
+
+/* ref smoother.cpp:400-465: fine-only nodes of even circle rings (odd t),
+ * then of even spokes (odd rings), pointwise with 3/4 f */
+static void extrapolated_pointwise(const Solver* S, const Level* l, double* u, const double* fhat) {
+    const Grid* g = &l->g;
+    const int nt = g->nt, N = g->nr - 1, split = g->split;
+    const int origin_pairs = S->boundary == 0;
+    const int even_rings = (split + 1) / 2;
+    Row r;
+    for (int i = 0; i < even_rings; ++i) {
+        const int s = 2 * i;
+        if (s == 0 && origin_pairs) continue;
+        const int base = s * nt;
+        if (is_dir(S, l, s)) {
+            for (int t = 1; t < nt; t += 2) u[base + t] = fhat[base + t];
+            continue;
+        }
+        for (int t = 1; t < nt; t += 2) {
+            const int p = base + t;
+            build_row(S, l, s, t, 1, &r);
+            double diag = 1.0;
+            double acc = 0.75 * fhat[p];
+            for (int e = 0; e < r.count; ++e) {
+                if (r.cols[e] == p) diag = r.vals[e];
+                else acc -= r.vals[e] * u[r.cols[e]];
+            }
+            u[p] = acc / diag;
+        }
+    }
+    if (split < g->nr) {
+        const int len = g->nr - split;
+        const int spokes = (nt + 1) / 2;
+        for (int i = 0; i < spokes; ++i) {
+            const int t = 2 * i;
+            for (int s = split % 2 == 0 ? split + 1 : split; s <= N; s += 2) {
+                const int p = split * nt + t * len + (s - split);
+                if (is_dir(S, l, s)) { u[p] = fhat[p]; continue; }
+                build_row(S, l, s, t, 1, &r);
+                double diag = 1.0;
+                double acc = 0.75 * fhat[p];
+                for (int e = 0; e < r.count; ++e) {
+                    if (r.cols[e] == p) diag = r.vals[e];
+                    else acc -= r.vals[e] * u[r.cols[e]];
+                }
+                u[p] = acc / diag;
+            }
+        }
+    }
+}
+
+/* ref smoother.cpp:467-503: antipodal fine-only pairs of the origin ring */
+static void extrapolated_origin_pairs(const Solver* S, const Level* l, double* u, const double* fhat) {
+    const Grid* g = &l->g;
+    const int nt = g->nt, half = nt / 2;
+    Row r;
+    for (int i = 0; i < half / 2; ++i) {
+        const int t = 2 * i + 1, t2 = t + half;
+        const int p = gidx(g, 0, t), q = gidx(g, 0, t2);
+        double a11 = 1.0, a12 = 0.0, a21 = 0.0, a22 = 1.0, b1, b2;
+        build_row(S, l, 0, t, 1, &r);
+        b1 = 0.75 * fhat[p];
+        for (int e = 0; e < r.count; ++e) {
+            const int c = r.cols[e];
+            if (c == p) a11 = r.vals[e];
+            else if (c == q) a12 = r.vals[e];
+            else b1 -= r.vals[e] * u[c];
+        }
+        build_row(S, l, 0, t2, 1, &r);
+        b2 = 0.75 * fhat[q];
+        for (int e = 0; e < r.count; ++e) {
+            const int c = r.cols[e];
+            if (c == q) a22 = r.vals[e];
+            else if (c == p) a21 = r.vals[e];
+            else b2 -= r.vals[e] * u[c];
+        }
+        const double det = a11 * a22 - a12 * a21;
+        u[p] = (b1 * a22 - a12 * b2) / det;
+        u[q] = (a11 * b2 - a21 * b1) / det;
+    }
+}
+
+/* ref smoother.cpp:83-91 */
+static void smooth_extrapolated(const Solver* S, const Level* l, double* u, const double* fhat) {
+    sweep_circle_x(S, l, 1, u, fhat, S->work, 1);
+    if (l->g.split < l->g.nr) sweep_radial_x(S, l, 1, u, fhat, 1);
+    extrapolated_pointwise(S, l, u, fhat);
+    if (S->boundary == 0) extrapolated_origin_pairs(S, l, u, fhat);
 }
 
 /* ref smoother.cpp:72-81 */
@@ -955,6 +1051,18 @@ static void restrict_t(const Grid* fine, const Grid* coarse, const double* fr, d
 
 /* ------------------------------------------------------------- multigrid */
 /* ref multigrid.cpp:48-59 */
+/* ref interpolation.cpp:145-165 */
+static void inject(const Grid* fine, const Grid* coarse, const double* fu, double* cu) {
+    for (int sc = 0; sc < coarse->nr; ++sc)
+        for (int tc = 0; tc < coarse->nt; ++tc)
+            cu[gidx(coarse, sc, tc)] = fu[gidx(fine, 2 * sc, 2 * tc)];
+}
+static void inject_transpose_add(const Grid* fine, const Grid* coarse, const double* cu, double* fu) {
+    for (int sc = 0; sc < coarse->nr; ++sc)
+        for (int tc = 0; tc < coarse->nt; ++tc)
+            fu[gidx(fine, 2 * sc, 2 * tc)] += cu[gidx(coarse, sc, tc)];
+}
+
 double orc_norm(int type, const double* v, long n) {
     if (type == 2) {
         double m = 0.0;
@@ -1101,6 +1209,41 @@ static void mask_dirichlet(const Solver* S, const Level* l, double* v) {
         for (int t = 0; t < l->g.nt; ++t) v[gidx(&l->g, 0, t)] = 0.0;
 }
 
+/* ref multigrid.cpp:224-248: r = fhat - (4/3 A0 u - I^T (1/3) A1 I u), Dirichlet rows f - u */
+static void extrapolated_residual(Solver* S, double* out) {
+    Level* l0 = &S->lv[0];
+    Level* l1 = &S->lv[1];
+    const Grid* g0 = &l0->g;
+    const long n0 = (long)g0->nr * g0->nt, n1 = (long)l1->g.nr * l1->g.nt;
+    apply_op(S, l0, S->mode, l0->u, out);
+    inject(g0, &l1->g, l0->u, l1->u);
+    apply_op(S, l1, S->mode, l1->u, l1->res);
+    for (long p = 0; p < n0; ++p) out[p] = l0->f[p] - (4.0 / 3.0) * out[p];
+    for (long p = 0; p < n1; ++p) l1->res[p] *= 1.0 / 3.0;
+    inject_transpose_add(g0, &l1->g, l1->res, out);
+    const int N = g0->nr - 1;
+    for (int t = 0; t < g0->nt; ++t) {
+        const int p = gidx(g0, N, t);
+        out[p] = l0->f[p] - l0->u[p];
+    }
+    if (S->boundary == 1)
+        for (int t = 0; t < g0->nt; ++t) {
+            const int p = gidx(g0, 0, t);
+            out[p] = l0->f[p] - l0->u[p];
+        }
+}
+
+/* ref multigrid.cpp:159-168: fhat = 4/3 f0 - I^T (1/3) f1 */
+static void build_extrapolated_rhs(Solver* S) {
+    Level* l0 = &S->lv[0];
+    Level* l1 = &S->lv[1];
+    const long n0 = (long)l0->g.nr * l0->g.nt, n1 = (long)l1->g.nr * l1->g.nt;
+    for (long p = 0; p < n0; ++p) l0->f[p] *= 4.0 / 3.0;
+    for (long p = 0; p < n1; ++p) l1->res[p] = -l1->f[p] / 3.0;
+    inject_transpose_add(&l0->g, &l1->g, l1->res, l0->f);
+    set_dirichlet_rows(S, l0, l0->f);
+}
+
 /* ref multigrid.cpp:183-220 */
 static void cycle(Solver* S, int lev, int type) {
     Level* l = &S->lv[lev];
@@ -1111,8 +1254,13 @@ static void cycle(Solver* S, int lev, int type) {
         return;
     }
     Level* c = &S->lv[lev + 1];
-    for (int i = 0; i < S->pre; ++i) smooth(S, l, l->u, l->f);
-    residual(S, l, S->mode, l->u, l->f, l->res);
+    const int ex = lev == 0 && S->ex;  /* smooth_level (multigrid.cpp:170-181) */
+    for (int i = 0; i < S->pre; ++i) {
+        if (ex) smooth_extrapolated(S, l, l->u, l->f);
+        else smooth(S, l, l->u, l->f);
+    }
+    if (ex) extrapolated_residual(S, l->res);
+    else residual(S, l, S->mode, l->u, l->f, l->res);
     restrict_t(&l->g, &c->g, l->res, c->f);
     mask_dirichlet(S, c, c->f);
     memset(c->u, 0, sizeof(double) * c->g.nr * c->g.nt);
@@ -1120,13 +1268,17 @@ static void cycle(Solver* S, int lev, int type) {
     else if (type == 1) { cycle(S, lev + 1, 1); cycle(S, lev + 1, 1); }
     else { cycle(S, lev + 1, 2); cycle(S, lev + 1, 0); }
     prolongate(&l->g, &c->g, c->u, l->u, 1);
-    for (int i = 0; i < S->post; ++i) smooth(S, l, l->u, l->f);
+    for (int i = 0; i < S->post; ++i) {
+        if (ex) smooth_extrapolated(S, l, l->u, l->f);
+        else smooth(S, l, l->u, l->f);
+    }
 }
 
 /* ref multigrid.cpp:267-275 */
 static double residual_norm(Solver* S) {
     Level* l = &S->lv[0];
-    residual(S, l, S->mode, l->u, l->f, l->res);
+    if (S->ex) extrapolated_residual(S, l->res);
+    else residual(S, l, S->mode, l->u, l->f, l->res);
     return orc_norm(S->norm, l->res, (long)l->g.nr * l->g.nt);
 }
 
@@ -1149,6 +1301,7 @@ static int fmg_initialize(Solver* S) {
         prolongate(&l->g, &c->g, c->u, l->u, 0);
         set_dirichlet_rows(S, l, l->u);
         if ((rc = assemble_rhs(S, l, l->f))) return rc;
+        if (lf == 0 && S->ex) build_extrapolated_rhs(S);
         for (int k = 0; k < S->fmg_it; ++k) {
             cycle(S, lf, S->fmg_cycle);
             if (lf == 0) ++S->fmg_run;
@@ -1214,10 +1367,11 @@ static int level_init(Solver* S, Level* l) {
     return 0;
 }
 
-static _Thread_local int g_extra[4]; /* solution, fmg, fmg_iterations, fmg_cycle */
+static _Thread_local int g_extra[5]; /* solution, fmg, fmg_iterations, fmg_cycle, extrapolation */
 static _Thread_local int g_extra_set;
-int orc_set_extra(int solution, int fmg, int fmg_iterations, int fmg_cycle) {
+int orc_set_extra(int solution, int fmg, int fmg_iterations, int fmg_cycle, int extrapolation) {
     g_extra[0] = solution; g_extra[1] = fmg; g_extra[2] = fmg_iterations; g_extra[3] = fmg_cycle;
+    g_extra[4] = extrapolation;
     g_extra_set = 1;
     return 0;
 }
@@ -1246,6 +1400,7 @@ int orc_create(int geom_kind, double kappa_eps, double delta_e, int alpha_coeff,
     S->fmg_it = 2; S->fmg_cycle = 2;
     if (g_extra_set) {
         S->sol = g_extra[0]; S->fmg = g_extra[1]; S->fmg_it = g_extra[2]; S->fmg_cycle = g_extra[3];
+        S->ex = g_extra[4];
         g_extra_set = 0;
     }
     Grid g0;
@@ -1453,6 +1608,10 @@ int orc_solve_native(void* h, double* u_out, double* history, int* iterations,
         if ((rc = fmg_initialize(S))) return rc;
     } else {
         if ((rc = assemble_rhs(S, l0, l0->f))) return rc;
+        if (S->ex) {
+            if ((rc = assemble_rhs(S, &S->lv[1], S->lv[1].f))) return rc;
+            build_extrapolated_rhs(S);
+        }
         memset(l0->u, 0, sizeof(double) * n);
         set_dirichlet_rows(S, l0, l0->u);
     }

@@ -38,8 +38,9 @@ int orc_solve(void* h, const double* f, double* u_out, double* history,
               double* seconds);
 double orc_norm(int type, const double* v, long n);
 /* extras for the next orc_create on this thread: manufactured solution
- * (0 None, 1 PolarOscillation) and FMG settings (multigrid.hpp:42-45) */
-int orc_set_extra(int solution, int fmg, int fmg_iterations, int fmg_cycle);
+ * (0 None, 1 PolarOscillation), FMG settings (multigrid.hpp:42-45) and
+ * implicit extrapolation (multigrid.hpp:41) */
+int orc_set_extra(int solution, int fmg, int fmg_iterations, int fmg_cycle, int extrapolation);
 int orc_solve_native(void* h, double* u_out, double* history, int* iterations,
                      int* fine_cycles, int* converged, double* mean_reduction,
                      double* err_weighted, double* err_inf);

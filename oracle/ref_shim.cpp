@@ -76,10 +76,11 @@ extern "C" {
 const char* ref_last_error() { return g_err.c_str(); }
 
 // extras for the next ref_create on this thread: manufactured solution
-// (0 None, 1 PolarOscillation, problem.hpp:32-44) and the FMG settings
-// (multigrid.hpp:42-45)
-thread_local int g_extra[4] = {0, 0, 2, 2};
-int ref_set_extra(int solution, int fmg, int fmg_iterations, int fmg_cycle) {
+// (0 None, 1 PolarOscillation, problem.hpp:32-44), the FMG settings
+// (multigrid.hpp:42-45) and implicit extrapolation (multigrid.hpp:41)
+thread_local int g_extra[5] = {0, 0, 2, 2, 0};
+int ref_set_extra(int solution, int fmg, int fmg_iterations, int fmg_cycle, int extrapolation) {
+    g_extra[4] = extrapolation;
     g_extra[0] = solution;
     g_extra[1] = fmg;
     g_extra[2] = fmg_iterations;
@@ -132,6 +133,8 @@ int ref_create(int geom_kind, double kappa_eps, double delta_e, int alpha_coeff,
         s.fmg = g_extra[1] != 0;
         s.fmg_iterations = g_extra[2];
         s.fmg_cycle = static_cast<CycleType>(g_extra[3]);
+        s.extrapolation = g_extra[4] != 0;
+        g_extra[4] = 0;
         g_extra[0] = 0;
         g_extra[1] = 0;
         g_extra[2] = 2;

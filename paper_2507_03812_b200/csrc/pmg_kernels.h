@@ -230,6 +230,24 @@ void launch_set_dirichlet(const LevelView& L, const RhsTables& T, double* u, cud
 int launch_exact_errors(const LevelView& L, const RhsTables& T, const double* u,
                         double* partials, int cap, cudaStream_t st);
 
+// ---- implicit extrapolation (pmg_extrap.cu) ----
+// g = 3/4 f (f on Dirichlet rows): RHS of the extrapolated line sweeps
+void launch_ex_fhat(const LevelView& L, const double* f, double* g, const int* active,
+                    cudaStream_t st);
+// extrapolated_pointwise + extrapolated_origin_pairs (smoother.cpp:400-503)
+void launch_ex_pointwise(const LevelView& L, bool onfly, double* u, const double* f,
+                         const int* active, cudaStream_t st);
+// inject (interpolation.cpp:145-154)
+void launch_inject(const LevelView& F, const LevelView& C, const double* fu, double* cu,
+                   const int* active, cudaStream_t st);
+// extrapolated_residual combination (multigrid.cpp:231-247); out holds A0 u0
+void launch_ex_residual(const LevelView& F, const LevelView& C, const double* u0,
+                        const double* f0, const double* a1, double* out, const int* active,
+                        cudaStream_t st);
+// build_extrapolated_rhs up to set_dirichlet_rows (multigrid.cpp:159-167)
+void launch_ex_rhs(const LevelView& F, const LevelView& C, double* f0, const double* f1,
+                   cudaStream_t st);
+
 // assembled rows [B][10][n] of a coarse-tail level (see k_rows)
 void launch_rows(const LevelView& L, bool onfly, double* rows, cudaStream_t st);
 // f = A u on the finest level for seeded RHS (same as launch_apply mode 0)

@@ -330,6 +330,8 @@ struct Solver {
                can_coarsen(grids.back(), tol))
             grids.push_back(coarsen(grids.back(), tol));
         const int L = static_cast<int>(grids.size());
+        if (set.extrapolation && L < 2)
+            throw PmgError(PMG_EINVAL, "extrapolation requires at least two levels");
         lv.resize(L);
         onfly = set.stencil_mode == 1 && !set.cache_geometry;
         serial = set.reference_order != 0;
@@ -342,6 +344,7 @@ struct Solver {
         }
         setup_coarse_tail();
         setup_mid();
+        if (set.extrapolation) ex_g = alloc<double>((size_t)B * lv[0].v.n);
         // convergence state
         hist_cap = std::max(set.max_iterations, 0) + 1;
         norms = alloc<double>(B);
@@ -530,6 +533,7 @@ struct Solver {
             start = l;
         }
         if (L - start > kMaxCoarse) start = L - kMaxCoarse;
+        if (set.extrapolation && start < 1) start = 1;  // level 0 runs the extrapolated kernels
         if (start >= L - 1) return;  // only the coarsest: nothing to gain
         coarse_start = start;
         std::memset(&coarse_params, 0, sizeof coarse_params);
@@ -693,7 +697,8 @@ struct Solver {
         if (const char* e = std::getenv("PMG_MID_SECTIONS")) max_b = std::atoi(e);
         if (max_nodes <= 0 || B > max_b) return;
         int first = coarse_start;
-        while (first - 1 >= 0 && coarse_start - (first - 1) <= kMaxMid) {
+        const int lowest = set.extrapolation ? 1 : 0;
+        while (first - 1 >= lowest && coarse_start - (first - 1) <= kMaxMid) {
             const HostGrid& g = lv[first - 1].g;
             if (!(g.nt() <= 256 && g.nr() - g.split <= 256 && g.uniform_angles &&
                   g.n() <= max_nodes))
@@ -943,8 +948,23 @@ struct Solver {
     }
 
     // ------------------------------------------------------------ cycle
+    // smooth_level (multigrid.cpp:170-181): level 0 with extrapolation runs
+    // smooth_extrapolated (smoother.cpp:83-91)
     void smooth(int l, const int* act) {
         Level& V = lv[l];
+        if (l == 0 && set.extrapolation) {
+            run(KK_OTHER, 1, [&] { launch_ex_fhat(V.v, V.f, ex_g, act, stream); });
+            run(KK_CIRCLE, line_launches(V.v, serial, onfly, exact_rings, 0, 1), [&] {
+                launch_circle(V.v, onfly, V.u, ex_g, V.cil, V.cm, V.corner, V.cz, V.of(), 1,
+                              serial, exact_rings, act, stream);
+            });
+            if (V.v.len > 0)
+                run(KK_RADIAL, 1, [&] {
+                    launch_radial(V.v, onfly, V.u, ex_g, V.ril, V.rm, 1, serial, act, stream);
+                });
+            run(KK_SMOOTH, 3, [&] { launch_ex_pointwise(V.v, onfly, V.u, V.f, act, stream); });
+            return;
+        }
         for (int parity = 0; parity < 2; ++parity)
             run(KK_CIRCLE, line_launches(V.v, serial, onfly, exact_rings, 0, parity), [&] {
                 launch_circle(V.v, onfly, V.u, V.f, V.cil, V.cm, V.corner, V.cz, V.of(), parity,
@@ -956,8 +976,28 @@ struct Solver {
                     launch_radial(V.v, onfly, V.u, V.f, V.ril, V.rm, parity, serial, act, stream);
                 });
     }
+    // extrapolated_residual (multigrid.cpp:224-248) into lv[0].res
+    void ex_residual(const int* act) {
+        Level& F = lv[0];
+        Level& C = lv[1];
+        run(KK_RESIDUAL, 2 * apply_launches(F.v) + 2, [&] {
+            launch_apply(F.v, onfly, 0, F.u, nullptr, F.res, nullptr, 0, act, stream);
+            launch_inject(F.v, C.v, F.u, C.u, act, stream);
+            launch_apply(C.v, onfly, 0, C.u, nullptr, C.res, nullptr, 0, act, stream);
+            launch_ex_residual(F.v, C.v, F.u, F.f, C.res, F.res, act, stream);
+        });
+    }
+    // build_extrapolated_rhs (multigrid.cpp:159-168)
+    void build_extrapolated_rhs() {
+        run(KK_OTHER, 1, [&] { launch_ex_rhs(lv[0].v, lv[1].v, lv[0].f, lv[1].f, stream); });
+        set_dirichlet_rows(0, lv[0].f);
+    }
     void residual(int l, const int* act) {
         Level& V = lv[l];
+        if (l == 0 && set.extrapolation) {
+            ex_residual(act);
+            return;
+        }
         run(KK_RESIDUAL, apply_launches(V.v), [&] {
             launch_apply(V.v, onfly, 1, V.u, V.f, V.res, nullptr, 0, act, stream);
         });
@@ -1017,10 +1057,17 @@ struct Solver {
     void norm_check() {
         Level& V = lv[0];
         int nb = 0;
-        run(KK_RESIDUAL, apply_launches(V.v), [&] {
-            nb = launch_apply(V.v, onfly, 1, V.u, V.f, V.res, partials, set.norm_type, active,
-                              stream);
-        });
+        if (set.extrapolation) {  // residual_norm (multigrid.cpp:267-275)
+            ex_residual(active);
+            run(KK_NORM, 1, [&] {
+                nb = launch_norm_partials(V.res, V.v.n, B, set.norm_type, partials, stream);
+            });
+        } else {
+            run(KK_RESIDUAL, apply_launches(V.v), [&] {
+                nb = launch_apply(V.v, onfly, 1, V.u, V.f, V.res, partials, set.norm_type, active,
+                                  stream);
+            });
+        }
         run(KK_NORM, 2, [&] {
             launch_norm_final(partials, nb, B, V.v.n, set.norm_type, norms, stream);
             ConvState cs{r0, hist, active, iters, conv, remaining, count, hist_cap};
@@ -1071,6 +1118,7 @@ struct Solver {
     std::vector<RhsTables> rhs_tabs;
     int* d_bad = nullptr;
     int fmg_run = 0;
+    double* ex_g = nullptr;  // 3/4 f of the extrapolated line sweeps (level 0)
 
     void build_rhs_tables() {
         if (!rhs_tabs.empty()) return;
@@ -1162,6 +1210,7 @@ struct Solver {
                 [&] { launch_prolong(F.v, C.v, F.w, C.u, F.u, false, active, stream); });
             set_dirichlet_rows(lf, F.u);
             assemble_level_rhs(lf);
+            if (lf == 0 && set.extrapolation) build_extrapolated_rhs();
             for (int c = 0; c < set.fmg_iterations; ++c) {
                 cycle(lf, set.fmg_cycle, active);
                 if (lf == 0) ++fmg_run;
@@ -1200,6 +1249,11 @@ struct Solver {
             run(KK_OTHER, 1, [&] { launch_set_active(active, count, conv, remaining, B, stream); });
             fmg_initialize();
         } else {  // multigrid.cpp:309-316 (the RHS is the current f)
+            if (set.extrapolation) {  // the extrapolated RHS needs f on levels 0 and 1
+                assemble_level_rhs(0);
+                assemble_level_rhs(1);
+                build_extrapolated_rhs();
+            }
             run(KK_OTHER, 2, [&] {
                 launch_set_active(active, count, conv, remaining, B, stream);
                 launch_fill(V.u, (long)B * V.v.n, 0.0, stream);
@@ -1337,9 +1391,9 @@ static void validate(const pmg_geometry* g, const pmg_problem* p, const pmg_grid
     if (s->extrapolation != 0 && s->extrapolation != 1)
         throw PmgError(PMG_EINVAL, "extrapolation=" + std::to_string(s->extrapolation) +
                                        " is not supported by this solver (use 0 or 1)");
-    if (s->extrapolation == 1)
+    if (s->extrapolation == 1 && s->max_levels == 1)
         throw PmgError(PMG_EINVAL,
-                       "extrapolation=1 is not supported by the B200 solve path yet");
+                       "extrapolation requires at least two levels (maxLevels=1 given)");
     if (s->fmg && (s->fmg_cycle < 0 || s->fmg_cycle > 2))
         throw PmgError(PMG_EINVAL, "unknown FMG_cycle type (expected V, W, or F)");
     if (p->solution < 0 || p->solution > 1)

@@ -2,7 +2,7 @@
 unmodified reference (oracle/_ref/libpolarmg_ref.so, built from
 /root/reference by oracle/Makefile).  Run in the build container:
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py [--all]   (missing fixtures only, or all)
 
 Every array is in the reference's NodeIndexing order.  Inputs are seeded
 (numpy default_rng / std::mt19937 seeds noted per key).
@@ -41,6 +41,9 @@ PROBLEM_CASES = {
     "problem_czarny_97x128_give_fmgV": Case(geometry="Czarny", kappa_eps=0.3, delta_e=1.4, a=97,
                                             b=128, stencil_mode="Give", fmg=1, fmg_cycle="V",
                                             fmg_iterations=1, rel_tol=1e-8, **POLAR),
+    "problem_czarny_49x64_extrapolated": Case(geometry="Czarny", kappa_eps=0.3, delta_e=1.4, a=49,
+                                              b=64, extrapolation=1, rel_tol=1e-11,
+                                              **dict(POLAR, max_iterations=400)),
 }
 
 
@@ -95,6 +98,8 @@ def make(name, c):
 
 if __name__ == "__main__":
     for name, c in CASES.items():
-        make(name, c)
+        if not os.path.exists(os.path.join(HERE, f"{name}.npz")) or "--all" in sys.argv:
+            make(name, c)
     for name, c in PROBLEM_CASES.items():
-        make_problem(name, c)
+        if not os.path.exists(os.path.join(HERE, f"{name}.npz")) or "--all" in sys.argv:
+            make_problem(name, c)

@@ -110,9 +110,15 @@ def test_create_fails_loudly_without_gpu():
 def test_invalid_settings_rejected_before_device():
     geom, prob, grid, st, _ = pmg.baseline_config(0)
     st.extrapolation = True
-    with pytest.raises(ValueError, match="extrapolation"):
+    st.max_levels = 1  # config.cpp:179-181
+    with pytest.raises(ValueError, match="extrapolation requires at least two levels"):
         pmg.MultigridSolver(geom, prob, grid, st)
     st.extrapolation = False
+    st.max_levels = 0
+    st.fmg_iterations = 0  # config.cpp:175-176
+    with pytest.raises(ValueError, match="FMG_iterations"):
+        pmg.MultigridSolver(geom, prob, grid, st)
+    st.fmg_iterations = 2
     st.pre_smoothing = -1
     with pytest.raises(ValueError, match="preSmoothingSteps"):
         pmg.MultigridSolver(geom, prob, grid, st)

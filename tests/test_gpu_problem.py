@@ -47,7 +47,8 @@ def gpu_solver(c: Case, reference_order=False):
                                cycle=c.cycle, max_iterations=c.max_iterations,
                                absolute_tolerance=c.abs_tol, relative_tolerance=c.rel_tol,
                                fmg=bool(c.fmg), fmg_iterations=c.fmg_iterations,
-                               fmg_cycle=c.fmg_cycle, reference_order=reference_order)
+                               fmg_cycle=c.fmg_cycle, extrapolation=bool(c.extrapolation),
+                               reference_order=reference_order)
     return pmg.MultigridSolver(geom, prob, grid, st)
 
 
@@ -100,6 +101,13 @@ SOLVE_CASES = {
                                   boundary_mode=1),
     "circle-fmgW-give": mk("CirclePolar", beta_coeff=0, stencil_mode="Give", fmg=1,
                            fmg_cycle="W"),
+    # implicit extrapolation (acceptance.cpp:63-75 settings)
+    "czarny-extrap": mk("Czarny", extrapolation=1, rel_tol=1e-11, max_iterations=400),
+    "shafranov-extrap-interior-give": mk("Shafranov", extrapolation=1, boundary_mode=1,
+                                         stencil_mode="Give", rel_tol=1e-11,
+                                         max_iterations=400),
+    "czarny97-extrap-fmgF": mk("Czarny", a=97, b=128, extrapolation=1, fmg=1, rel_tol=1e-11,
+                               max_iterations=400),
 }
 
 
@@ -110,8 +118,8 @@ def solved(request):
     c = SOLVE_CASES[name]
     ref = Checker(c).solve_native()
     gpu = gpu_solver(c, reference_order=ro)
-    if not c.fmg:
-        gpu.assemble_rhs()
+    if not c.fmg and not c.extrapolation:
+        gpu.assemble_rhs()  # FMG / extrapolation assemble inside solve(), like the reference
     rep = gpu.solve()
     return ro, c, ref, rep, gpu.solution()
 

@@ -70,10 +70,13 @@ def test_polar_oscillation_kats():
 @pytest.mark.parametrize("geo", ["CirclePolar", "Shafranov", "Czarny"])
 @pytest.mark.parametrize("bm", [0, 1])
 @pytest.mark.parametrize("fmg", [0, 1])
-def test_oracle_problem_vs_reference(geo, bm, fmg):
+@pytest.mark.parametrize("ex", [0, 1], ids=["plain", "extrapolated"])
+def test_oracle_problem_vs_reference(geo, bm, fmg, ex):
     ke, de = {"CirclePolar": (0.0, 0.0), "Shafranov": (0.3, 0.2), "Czarny": (0.3, 1.4)}[geo]
     c = Case(geometry=geo, kappa_eps=ke, delta_e=de, a=33, b=64, R0=1.3e-5, solution=1,
-             alpha_jump=0.7, delta_r=0.05, boundary_mode=bm, fmg=fmg, max_iterations=150)
+             alpha_jump=0.7, delta_r=0.05, boundary_mode=bm, fmg=fmg, extrapolation=ex,
+             stencil_mode="Give" if (bm + fmg) % 2 else "Take", max_iterations=400,
+             rel_tol=1e-11 if ex else 1e-10)
     R, O = RefSolver(c), OracleSolver(c)
     assert np.array_equal(O.assemble_rhs(0), R.assemble_rhs(0))
     a, b = O.solve_native(), R.solve_native()
