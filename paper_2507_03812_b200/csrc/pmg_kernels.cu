@@ -40,6 +40,10 @@ constexpr unsigned FULL = 0xffffffffu;
 // The across-origin ring is solved in the reference's exact substitution
 // order (origin_solve_exact) in reference_order mode and for rings of at most
 // this length; longer rings use the parallel 2x2-map scan (origin_solve).
+// minimum resident CTAs of the cluster line kernels (register cap 64/thread at 4)
+#ifndef PMG_CL_MINB
+#define PMG_CL_MINB 4
+#endif
 #ifndef PMG_ORIGIN_SCAN_MIN
 #define PMG_ORIGIN_SCAN_MIN 0
 #endif
@@ -1355,7 +1359,7 @@ inline __device__ int cl_rows(int n, int C) {  // rows per CTA
 
 // Radial sweep with each spoke split over a cluster (fast mode, Take).
 template <int K>
-__global__ void __launch_bounds__(256) k_radial_cl(LevelView L, double* __restrict__ u,
+__global__ void __launch_bounds__(256, PMG_CL_MINB) k_radial_cl(LevelView L, double* __restrict__ u,
                                                    const double* __restrict__ f,
                                                    const double* __restrict__ ril,
                                                    const double* __restrict__ rm, int parity,
@@ -1443,7 +1447,7 @@ __global__ void __launch_bounds__(256) k_radial_cl(LevelView L, double* __restri
 // Circle sweep with each ring split over a cluster (fast mode); rings
 // s = s_first + 2*line; the across-origin ring is launched separately.
 template <bool ONFLY, int K>
-__global__ void __launch_bounds__(256) k_circle_cl(LevelView L, double* __restrict__ u,
+__global__ void __launch_bounds__(256, PMG_CL_MINB) k_circle_cl(LevelView L, double* __restrict__ u,
                                                    const double* __restrict__ f,
                                                    const double* __restrict__ cil,
                                                    const double* __restrict__ cm,

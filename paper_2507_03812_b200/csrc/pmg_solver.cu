@@ -204,6 +204,9 @@ struct Solver {
     // convergence state
     double *norms = nullptr, *partials = nullptr, *r0 = nullptr, *hist = nullptr;
     int *active = nullptr, *iters = nullptr, *conv = nullptr, *remaining = nullptr;
+    // the per-section activity mask the cycle kernels test; a single section
+    // is only cycled while it is active, so its kernels skip the dependent load
+    const int* act_mask() const { return B > 1 ? active : nullptr; }
     int* count = nullptr;
     // single-launch coarse tail: levels >= coarse_start run in k_coarse_cycle
     int coarse_start = -1;
@@ -1058,13 +1061,13 @@ struct Solver {
         Level& V = lv[0];
         int nb = 0;
         if (set.extrapolation) {  // residual_norm (multigrid.cpp:267-275)
-            ex_residual(active);
+            ex_residual(act_mask());
             run(KK_NORM, 1, [&] {
                 nb = launch_norm_partials(V.res, V.v.n, B, set.norm_type, partials, stream);
             });
         } else {
             run(KK_RESIDUAL, apply_launches(V.v), [&] {
-                nb = launch_apply(V.v, onfly, 1, V.u, V.f, V.res, partials, set.norm_type, active,
+                nb = launch_apply(V.v, onfly, 1, V.u, V.f, V.res, partials, set.norm_type, act_mask(),
                                   stream);
             });
         }
@@ -1083,7 +1086,7 @@ struct Solver {
         const long long l0 = launches;
         cudaGraph_t g = nullptr;
         PMG_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-        cycle(0, set.cycle, active);
+        cycle(0, set.cycle, act_mask());
         norm_check();
         PMG_CUDA(cudaStreamEndCapture(stream, &g));
         PMG_CUDA(cudaGraphInstantiate(&cycle_exec, g, 0));
@@ -1202,17 +1205,17 @@ struct Solver {
     void fmg_initialize() {
         const int L = static_cast<int>(lv.size());
         assemble_level_rhs(L - 1);
-        coarse(L - 1, active);
+        coarse(L - 1, act_mask());
         for (int lf = L - 2; lf >= 0; --lf) {
             Level& F = lv[lf];
             Level& C = lv[lf + 1];
             run(KK_PROLONG, 1,
-                [&] { launch_prolong(F.v, C.v, F.w, C.u, F.u, false, active, stream); });
+                [&] { launch_prolong(F.v, C.v, F.w, C.u, F.u, false, act_mask(), stream); });
             set_dirichlet_rows(lf, F.u);
             assemble_level_rhs(lf);
             if (lf == 0 && set.extrapolation) build_extrapolated_rhs();
             for (int c = 0; c < set.fmg_iterations; ++c) {
-                cycle(lf, set.fmg_cycle, active);
+                cycle(lf, set.fmg_cycle, act_mask());
                 if (lf == 0) ++fmg_run;
             }
         }
@@ -1278,7 +1281,7 @@ struct Solver {
                 PMG_CUDA(cudaGraphLaunch(cycle_exec, stream));
                 launches += cycle_nodes;
             } else {
-                cycle(0, set.cycle, active);
+                cycle(0, set.cycle, act_mask());
                 norm_check();
             }
             ++it;
