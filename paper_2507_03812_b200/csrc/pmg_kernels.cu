@@ -1826,6 +1826,24 @@ template <int KW, bool CG>
 __device__ void origin_warp(const CoarseLevel& C, double* __restrict__ U,
                             const double* __restrict__ F, long off, int b) {
     const LevelView& L = C.v;
+    if (C.of.inv && L.nt <= 32) {  // tiny ring: dense inverse, u_i = sum_j Ainv_ij rhs_j
+        const int n = L.nt, lane = threadIdx.x & 31;
+        const double* Rw = C.rows + (long)b * 10 * L.n;
+        const double r = lane < n ? circle_rhs<CG>(L, Rw, U, F, 0, lane) : 0.0;
+        const double* A = C.of.inv + (long)b * n * n;
+        double a0 = 0.0, a1 = 0.0;
+        for (int j = 0; j < n; j += 2) {
+            const double r0 = __shfl_sync(FULL, r, j);
+            const double r1 = __shfl_sync(FULL, r, j + 1 < n ? j + 1 : j);
+            if (lane < n) {
+                a0 += A[(long)j * n + lane] * r0;
+                if (j + 1 < n) a1 += A[(long)(j + 1) * n + lane] * r1;
+            }
+        }
+        __syncwarp();
+        if (lane < n) U[lane] = a0 + a1;
+        return;
+    }
     const int n = L.nt, h = n / 2, nb = n - 2;
     const int KE = (n + 31) >> 5;  // rows per lane (<= KW)
     const int lane = threadIdx.x & 31, j0 = lane * KE;
@@ -1943,7 +1961,9 @@ __device__ void coarse_smooth(const CoarseLevel& C, int b, const Team& team) {
                 continue;
             }
             if (s == 0 && L.boundary == 0) {
+#ifndef PMG_EXP_NO_ORIGIN
                 origin_warp<KW, CG>(C, U, F, off, b);
+#endif
                 continue;
             }
             double y[KW];

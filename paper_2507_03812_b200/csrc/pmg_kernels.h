@@ -17,6 +17,8 @@ struct OriginFactor {
     const double* row2;   // [B][n] L(n-1,k), k in [fc2, n-1)
     const double* D;      // [B][n] LDL^T diagonal
     int fc1, fc2;
+    const double* inv;    // [B][n][n] dense inverse, column-major (rings of <= 32 nodes, the
+                          // one-block tail), or null
 };
 
 // Generic envelope factor with identity ordering (coarsest level).

@@ -179,6 +179,7 @@ struct Level {
     double* cz = nullptr;  // Sherman-Morrison vectors of the circle lines (exact path)
     double* rows = nullptr;  // assembled rows [B][10][n] (coarse-tail levels)
     double *ob1 = nullptr, *ob2 = nullptr, *or1 = nullptr, *or2 = nullptr, *oD = nullptr;
+    double* oinv = nullptr;  // dense inverse of the origin ring (n_theta <= 32)
     int ofc1 = 0, ofc2 = 0;
     Weights w{};
     EnvFactor env{};
@@ -520,6 +521,7 @@ struct Solver {
             if (!coarsest) {
                 d += 11 * n;                        // res, assembled rows
                 d += 2 * sp * nt + sp + 2 * nt * len + 5 * nt + 2 * nr + 2 * nt;
+                if (nt <= 32) d += nt * nt;  // origin ring inverse
             } else {
                 d += n <= 64 ? n * n : lv[l].env.nnz + n + n / 2 + n + 2;  // inv | L, D, fc, ro
             }
@@ -588,6 +590,10 @@ struct Solver {
                     c.of.D = static_cast<double*>(place(V.oD, nt * 8, nt, 8));
                     c.of.fc1 = V.ofc1;
                     c.of.fc2 = V.ofc2;
+                    // dense inverse on coarse levels only: on the finest level the
+                    // substitution's backward stability matters at the roundoff floor
+                    if (V.oinv && l > 0)
+                        c.of.inv = static_cast<double*>(place(V.oinv, nt * nt * 8, nt * nt, 8));
                 }
                 c.w.rwb = static_cast<double*>(place(V.w.rwb, 0, nr, 8));
                 c.w.rwa = static_cast<double*>(place(V.w.rwa, 0, nr, 8));
@@ -649,7 +655,7 @@ struct Solver {
                 const size_t o = c + offsetof(CoarseLevel, of);
                 for (size_t f : {offsetof(OriginFactor, band1), offsetof(OriginFactor, band2),
                                  offsetof(OriginFactor, row1), offsetof(OriginFactor, row2),
-                                 offsetof(OriginFactor, D)})
+                                 offsetof(OriginFactor, D), offsetof(OriginFactor, inv)})
                     mark(o + f);
                 const size_t w = c + offsetof(CoarseLevel, w);
                 for (size_t f : {offsetof(Weights, rwb), offsetof(Weights, rwa),
@@ -853,7 +859,7 @@ struct Solver {
             perm[2 * i + 1] = nt / 2 + i;
         }
         std::vector<double> b1((size_t)B * nt, 0.0), b2((size_t)B * nt, 0.0),
-            r1((size_t)B * nt, 0.0), r2((size_t)B * nt, 0.0), D((size_t)B * nt, 0.0);
+            r1((size_t)B * nt, 0.0), r2((size_t)B * nt, 0.0), D((size_t)B * nt, 0.0), oinv;
         for (int b = 0; b < B; ++b) {
             HostEnv E;
             E.factor(nt, assemble_coo(HL, V.g, b, nodes), perm);
@@ -877,7 +883,21 @@ struct Solver {
             }
             for (int k = 0; k < nt - 2; ++k) r1[o + k] = E.at(nt - 2, k);
             for (int k = 0; k < nt - 1; ++k) r2[o + k] = E.at(nt - 1, k);
+            if (nt <= 32) {  // dense inverse for the warp solves of the one-block tail
+                if (b == 0) oinv.assign((size_t)B * nt * nt, 0.0);
+                std::vector<double> y(nt);
+                for (int j = 0; j < nt; ++j) {
+                    for (int k = 0; k < nt; ++k) y[k] = perm[k] == j ? 1.0 : 0.0;
+                    for (int i = 0; i < nt; ++i)
+                        for (int k = E.fc[i]; k < i; ++k) y[i] -= E.at(i, k) * y[k];
+                    for (int i = 0; i < nt; ++i) y[i] /= E.D[i];
+                    for (int i = nt - 1; i >= 0; --i)
+                        for (int k = E.fc[i]; k < i; ++k) y[k] -= E.at(i, k) * y[i];
+                    for (int k = 0; k < nt; ++k) oinv[((size_t)b * nt + j) * nt + perm[k]] = y[k];
+                }
+            }
         }
+        V.oinv = oinv.empty() ? nullptr : upload(oinv);
         V.ob1 = upload(b1);
         V.ob2 = upload(b2);
         V.or1 = upload(r1);

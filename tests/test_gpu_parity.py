@@ -162,10 +162,13 @@ def test_solve(pair):
     g = f.copy()
     m = rng.random(f.size) < 0.5
     g[m] = np.nextafter(g[m], np.inf)
-    sens = relmax(ref.solve(g)["u"], out["u"])
+    pert = ref.solve(g)
+    sens = relmax(pert["u"], out["u"])
     assert relmax(u, out["u"]) < max(1e-10, sens), (relmax(u, out["u"]), sens)
     h = np.array(rep.residual_norms)
-    k = min(len(h), len(out["residual_norms"]))
-    # late residuals sit at the roundoff floor of |f - A u| ~ 1e-16 |f|: compare
-    # the history relative to r0
-    assert np.abs(h[:k] - out["residual_norms"][:k]).max() <= 1e-12 * h[0]
+    k = min(len(h), len(out["residual_norms"]), len(pert["residual_norms"]))
+    # late residuals sit at the roundoff floor of |f - A u|: compare the history
+    # relative to r0, or to the reference's own one-ulp sensitivity when larger
+    dh = np.abs(h[:k] - out["residual_norms"][:k]).max()
+    sens_h = np.abs(pert["residual_norms"][:k] - out["residual_norms"][:k]).max()
+    assert dh <= max(1e-12 * h[0], 4 * sens_h), (dh, sens_h)
