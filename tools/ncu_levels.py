@@ -13,7 +13,8 @@ for r in csv.DictReader(lines):
     short = (m.group(1) + (m.group(2) or "")) if m else name[:40]
     v = float(r["Metric Value"].replace(",", ""))
     unit = r["Metric Unit"]
-    us = v / 1000.0 if unit == "nsecond" else v * 1000.0 if unit == "msecond" else v
+    us = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3,
+          "msecond": 1e3}.get(unit, 1.0) * v
     rows.append((short, r["Grid Size"], r["Block Size"], us))
 agg = collections.OrderedDict()
 for k, g, b, us in rows:
