@@ -87,6 +87,7 @@ struct LevelView {
     const double* det;
     const double* rh;        // [nr-1] RN(1/h_s)  (exact reciprocals for xdiv)
     const double* rk;        // [nt]   RN(1/k_t)
+    const double* rows;      // [B][10][n] assembled rows (latency-bound levels) or null
     Geo geo;
 
     // reference NodeIndexing (polar_grid.hpp:24-27)

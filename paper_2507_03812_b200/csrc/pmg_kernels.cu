@@ -25,6 +25,20 @@ namespace pmg {
 
 namespace cg = cooperative_groups;
 
+#ifdef PMG_KTRACE
+// diagnostics build only: clock64 marks of thread 0 of block (0,0)
+__device__ unsigned long long g_ktrace[16];
+#define KT(i)                                                       \
+    do {                                                            \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) \
+            g_ktrace[i] = clock64();                                \
+    } while (0)
+#else
+#define KT(i) \
+    do {      \
+    } while (0)
+#endif
+
 // Programmatic dependent launch: every kernel of the solve lets the next one
 // in the stream start launching at once and waits for its predecessor's
 // results before touching them (griddepcontrol; no-ops without the launch
@@ -955,6 +969,7 @@ __global__ void __launch_bounds__(512) k_circle(LevelView L, double* __restrict_
                                                 OriginFactor of, int parity, int serial,
                                                 int exact_rings,
                                                 const int* __restrict__ active) {
+    KT(0);
     pdl_enter();
     extern __shared__ double smem[];
     const int b = blockIdx.y;
@@ -975,6 +990,33 @@ __global__ void __launch_bounds__(512) k_circle(LevelView L, double* __restrict_
     double* M = IL + pn;
     double* scr = M + pn;
     const CoefAt<ONFLY> cf{&L, off, b};
+    const bool origin = s == 0 && L.boundary == 0;
+    const long fo = (long)b * L.split * nt + (long)s * nt;
+    const bool exact = serial || s <= exact_rings;  // block-uniform
+    if (!origin) {  // line factors: asynchronous copies, overlapped with the rhs
+        for (int t = threadIdx.x; t < nt; t += T) {
+            __pipeline_memcpy_async(&IL[P(t)], &cil[fo + t], 8);
+            __pipeline_memcpy_async(&M[P(t)], &cm[fo + t], 8);
+        }
+        __pipeline_commit();
+    }
+    KT(1);
+    if (L.rows) {  // assembled rows (stencil.cpp:44-137 values, k_rows)
+        const double* Rw = L.rows + (long)b * 10 * L.n;
+        const int n = L.n;
+        for (int t = threadIdx.x; t < nt; t += T) {
+            const int p = base + t;
+            const Nbr q = neighbours(L, s, t, p);
+            double acc = F[p];
+            acc -= Rw[1 * n + p] * U[q.pSM];
+            acc -= Rw[2 * n + p] * U[q.pSP];
+            acc -= Rw[5 * n + p] * U[q.pSMTM];
+            acc -= Rw[6 * n + p] * U[q.pSMTP];
+            acc -= Rw[7 * n + p] * U[q.pSPTM];
+            acc -= Rw[8 * n + p] * U[q.pSPTP];
+            Y[P(t)] = acc;
+        }
+    } else
     for (int t = threadIdx.x; t < nt; t += T) {
         const int p = base + t;
         const Nbr q = neighbours(L, s, t, p);
@@ -992,26 +1034,27 @@ __global__ void __launch_bounds__(512) k_circle(LevelView L, double* __restrict_
         }
         Y[P(t)] = acc;
     }
-    if (s == 0 && L.boundary == 0) {
+    KT(2);
+    if (origin) {
         __syncthreads();
         if (serial || nt < PMG_ORIGIN_SCAN_MIN)
             origin_solve_exact(Y, IL, M, of, b, nt);
         else
             origin_solve<K>(Y, IL, of, b, nt, scr);
     } else {
-        const long fo = (long)b * L.split * nt + (long)s * nt;
-        const bool exact = serial || s <= exact_rings;  // block-uniform
-        for (int t = threadIdx.x; t < nt; t += T) {
-            IL[P(t)] = exact ? cil[fo + t] : __drcp_rn(cil[fo + t]);
-            M[P(t)] = cm[fo + t];
-        }
+        __pipeline_wait_prior(0);
+        if (!exact)  // each thread converts the elements it copied
+            for (int t = threadIdx.x; t < nt; t += T) IL[P(t)] = __drcp_rn(IL[P(t)]);
         __syncthreads();
+        KT(3);
         if (exact)
             cyc_solve_exact(Y, IL, M, nt, corner[(long)b * L.split + s], cz + fo, scr);
         else
             line_solve<K, true>(Y, IL, M, nt, corner[(long)b * L.split + s], scr);
     }
+    KT(4);
     for (int t = threadIdx.x; t < nt; t += T) U[base + t] = Y[P(t)];
+    KT(5);
 }
 
 // ------------------------------------------------------------- radial sweep
@@ -1025,6 +1068,7 @@ __global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict_
                                                 const double* __restrict__ ril,
                                                 const double* __restrict__ rm, int parity,
                                                 int serial, const int* __restrict__ active) {
+    KT(0);
     pdl_enter();
     extern __shared__ double smem[];
     const int b = blockIdx.y;
@@ -1042,17 +1086,36 @@ __global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict_
     double* scr = M + pn;
     const CoefAt<ONFLY> cf{&L, off, b};
     const long fo = ((long)b * L.nt + t) * len;
-    for (int i = threadIdx.x; i < len; i += T) {
-        const double lv = ril[fo + i];
-        IL[P(i)] = serial ? lv : __drcp_rn(lv);
-        M[P(i)] = rm[fo + i];
+    for (int i = threadIdx.x; i < len; i += T) {  // overlapped with the rhs
+        __pipeline_memcpy_async(&IL[P(i)], &ril[fo + i], 8);
+        __pipeline_memcpy_async(&M[P(i)], &rm[fo + i], 8);
     }
+    __pipeline_commit();
+    KT(1);
     // interior rows split < s < n_r-1 (Take): only the off-line couplings --
     // angular (att) and corner (art) -- with direct spoke-major offsets; all
     // operands of two rows are loaded before any arithmetic (memory-level
     // parallelism).  Same expressions as row_from, so bitwise identical.
     int ifirst = 1, ilast = len - 2;  // rows 0 (s = split) and len-1 (s = n_r-1) below
-    if (!ONFLY) {
+    if (L.rows) {  // assembled rows (k_rows): every row the same ten products
+        const double* Rw = L.rows + (long)b * 10 * L.n;
+        const int n = L.n;
+        for (int i = threadIdx.x; i < len; i += T) {
+            const int s = split + i, p = base + i;
+            const Nbr q = neighbours(L, s, t, p);
+            double acc = F[p];
+            if (s == split) acc -= Rw[1 * n + p] * U[q.pSM];
+            acc -= Rw[3 * n + p] * U[q.pTM];
+            acc -= Rw[4 * n + p] * U[q.pTP];
+            acc -= Rw[5 * n + p] * U[q.pSMTM];
+            acc -= Rw[6 * n + p] * U[q.pSMTP];
+            acc -= Rw[7 * n + p] * U[q.pSPTM];
+            acc -= Rw[8 * n + p] * U[q.pSPTP];
+            Y[P(i)] = acc;
+        }
+        ifirst = len;
+        ilast = -1;
+    } else if (!ONFLY) {
         const int tm = L.tminus(t), tp = L.tplus(t);
         const double km = L.k[tm], kp = L.k[t], rkm = L.rk[tm], rkp = L.rk[t];
         const int dTM = (tm - t) * len, dTP = (tp - t) * len;
@@ -1087,7 +1150,7 @@ __global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict_
         ifirst = len;  // Give: the general path below handles every row
         ilast = -1;
     }
-    for (int i = threadIdx.x; i < len; i += T) {
+    for (int i = threadIdx.x; i < len && !L.rows; i += T) {
         if (i >= ifirst && i <= ilast) continue;
         const int s = split + i;
         const int p = base + i;
@@ -1111,14 +1174,21 @@ __global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict_
         }
         Y[P(i)] = acc;
     }
+    __pipeline_wait_prior(0);
+    if (!serial)  // each thread converts the factor elements it copied
+        for (int i = threadIdx.x; i < len; i += T) IL[P(i)] = __drcp_rn(IL[P(i)]);
+    KT(2);
     __syncthreads();
+    KT(3);
     if (serial) {
         if (threadIdx.x == 0) tri_solve_exact(Y, IL, M, len);
         __syncthreads();
     } else {
         line_solve<K, false>(Y, IL, M, len, 0.0, scr);
     }
+    KT(4);
     for (int i = threadIdx.x; i < len; i += T) U[base + i] = Y[P(i)];
+    KT(5);
 }
 
 // ------------------------------------------------- cluster-split line solves
@@ -1821,6 +1891,21 @@ __device__ __forceinline__ double row_residual(const LevelView& L, const double*
     return ldv<CG>(F + (p)) - acc;
 }
 
+// r = f - A u from the assembled rows, one thread per node (latency-bound
+// levels; same products and order as apply_node)
+__global__ void __launch_bounds__(256) k_residual_rows(LevelView L, const double* __restrict__ u,
+                                                       const double* __restrict__ f,
+                                                       double* __restrict__ r,
+                                                       const int* __restrict__ active) {
+    pdl_enter();
+    const int b = blockIdx.y;
+    if (active && !active[b]) return;
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= L.n) return;
+    const long off = (long)b * L.n;
+    r[off + p] = row_residual<false>(L, L.rows + (long)b * 10 * L.n, u + off, f + off, p);
+}
+
 // warp version of origin_solve (2nd-order recurrences as 2x2-map scans)
 template <int KW, bool CG>
 __device__ void origin_warp(const CoarseLevel& C, double* __restrict__ U,
@@ -2433,6 +2518,10 @@ int apply_blocks(const LevelView& L) { return tile_geom(L).ntiles(); }
 int launch_apply(const LevelView& L, bool onfly, int mode, const double* u, const double* f,
                  double* out, double* partials, int norm_type, const int* active,
                  cudaStream_t st) {
+    if (L.rows && mode == 1 && !partials) {
+        launch_k(k_residual_rows, dim3((L.n + 255) / 256, L.B), 256, 0, st, L, u, f, out, active);
+        return 0;
+    }
     const TileGeom G = tile_geom(L);
     const int nb = G.ntiles();
     dim3 grid(nb, L.B);
@@ -2629,7 +2718,11 @@ void launch_radial(const LevelView& L, bool onfly, double* u, const double* f, c
     if (L.len <= 0) return;
     const int lines = (L.nt - parity + 1) / 2;
     int K, T;
-    if (!serial && !onfly && L.len > 1024) {
+    static const int cl_min = [] {
+        const char* e = std::getenv("PMG_RADIAL_CL_MIN");
+        return e ? std::atoi(e) : 1024;
+    }();
+    if (!serial && !onfly && L.len > cl_min) {
         int C = std::min(8, (L.len + 899) / 900);
         if (const char* e = std::getenv("PMG_LINE_CLUSTER_ROWS")) {
             const int rows = std::atoi(e);
@@ -2719,6 +2812,10 @@ void launch_flush(double* buf, long n, cudaStream_t st) {
 }  // namespace pmg
 
 namespace pmg {
+#ifdef PMG_KTRACE
+void read_ktrace(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_ktrace, sizeof(g_ktrace)); }
+#endif
+
 void launch_mid_cycle(const MidParams& mp, const int* prog, int nops, int B, const int* active,
                       cudaStream_t st) {
     const size_t sm = (size_t)mp.tail.smem_bytes;

@@ -111,6 +111,9 @@ struct MidParams {
     CoarseParams tail;
     unsigned long long* trace;  // PMG_TAIL_TRACE: %globaltimer per op (cluster 0, rank 0)
 };
+#ifdef PMG_KTRACE
+void read_ktrace(unsigned long long* out);  // diagnostics build only
+#endif
 void launch_mid_cycle(const MidParams& mp, const int* prog, int nops, int B, const int* active,
                       cudaStream_t st);
 // largest cluster size <= want (power of 2) that can be scheduled, 0 if none

@@ -346,6 +346,7 @@ struct Solver {
             V.g = std::move(grids[l]);
             setup_level(V, l == L - 1, bad);
         }
+        setup_rows();
         setup_coarse_tail();
         setup_mid();
         if (set.extrapolation) ex_g = alloc<double>((size_t)B * lv[0].v.n);
@@ -566,9 +567,12 @@ struct Solver {
             // the tail works from assembled rows: geometry/coefficients stay behind
             v.r = v.h = v.rh = v.k = v.rk = v.sn = v.cs = v.alpha = v.beta = nullptr;
             v.arr = v.art = v.att = v.det = nullptr;
+            v.rows = nullptr;
             if (!coarsest) {
-                V.rows = alloc<double>((size_t)B * 10 * n, false);
-                launch_rows(V.v, onfly, V.rows, stream);
+                if (!V.rows) {
+                    V.rows = alloc<double>((size_t)B * 10 * n, false);
+                    launch_rows(V.v, onfly, V.rows, stream);
+                }
                 c.rows = static_cast<double*>(place(V.rows, 10 * n * 8, 10 * n, 8));
             }
             c.u = static_cast<double*>(place(top ? V.u : nullptr, n * 8, n, 8));
@@ -693,6 +697,22 @@ struct Solver {
         }
         if (std::getenv("PMG_TAIL_TRACE"))
             coarse_params.trace = alloc<unsigned long long>(maxlen + 4);
+    }
+
+    // Latency-bound levels (all sections together at most PMG_ROWS_NODES nodes,
+    // level 0 excluded) keep their assembled rows: the line kernels and the
+    // residual then evaluate ten products per node instead of re-deriving the
+    // stencil (same values, k_rows).
+    void setup_rows() {
+        long max_nodes = 300000;
+        if (const char* e = std::getenv("PMG_ROWS_NODES")) max_nodes = std::atol(e);
+        for (size_t l = 1; l < lv.size(); ++l) {
+            Level& V = lv[l];
+            if ((long)B * V.v.n > max_nodes) continue;
+            V.rows = alloc<double>((size_t)B * 10 * V.v.n, false);
+            launch_rows(V.v, onfly, V.rows, stream);
+            V.v.rows = V.rows;
+        }
     }
 
     // Cluster-wide sub-cycle (k_mid_cycle): the levels just above the resident
@@ -845,6 +865,7 @@ struct Solver {
         h.beta = V.h_beta.data();
         h.arr = h.art = h.att = h.det = nullptr;
         h.rh = h.rk = nullptr;
+        h.rows = nullptr;
         return h;
     }
 
@@ -1686,6 +1707,13 @@ int pmg_solve(pmg_handle h, pmg_report* reports, double* history, int history_ca
     if (rc == PMG_ENOTCONV) pmg::g_err = "solve ended without meeting a tolerance";
     return rc;
 }
+
+#ifdef PMG_KTRACE
+int pmg_debug_ktrace(unsigned long long* out) {
+    pmg::read_ktrace(out);
+    return 0;
+}
+#endif
 
 int pmg_assemble_rhs(pmg_handle h) {
     return guarded([&] {
