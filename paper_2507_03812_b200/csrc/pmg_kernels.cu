@@ -27,15 +27,23 @@ namespace cg = cooperative_groups;
 
 #ifdef PMG_KTRACE
 // diagnostics build only: clock64 marks of thread 0 of block (0,0)
-__device__ unsigned long long g_ktrace[16];
+__device__ unsigned long long g_ktrace[32];
 #define KT(i)                                                       \
     do {                                                            \
         if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) \
             g_ktrace[i] = clock64();                                \
     } while (0)
+#define KTS(slot, i)                                                \
+    do {                                                            \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && (slot) >= 0) \
+            g_ktrace[16 + 5 * (slot) + (i)] = clock64();            \
+    } while (0)
 #else
 #define KT(i) \
     do {      \
+    } while (0)
+#define KTS(slot, i) \
+    do {             \
     } while (0)
 #endif
 
@@ -2037,6 +2045,9 @@ __device__ void coarse_smooth(const CoarseLevel& C, int b, const Team& team) {
     const int warp = team.warp(), nw = team.nwarps(), lane = threadIdx.x & 31;
     const int nt = L.nt;
     const double* Rw = C.rows + (long)b * 10 * L.n;
+    const int kslot = nt == 8 ? 0 : nt == 16 ? 1 : nt == 32 ? 2 : -1;
+    (void)kslot;
+    KTS(kslot, 0);
     for (int parity = 0; parity < 2; ++parity) {  // circle sweeps (smoother.cpp:95-116)
         const int lines = L.split > parity ? (L.split - parity + 1) / 2 : 0;
         for (int li = warp; li < lines; li += nw) {
@@ -2058,13 +2069,20 @@ __device__ void coarse_smooth(const CoarseLevel& C, int b, const Team& team) {
             for (int q = 0; q < KW; ++q)
                 y[q] = (q < KE && j0 + q < nt) ? circle_rhs<CG>(L, Rw, U, F, s, j0 + q) : 0.0;
             const long fo = (long)b * L.split * nt + (long)s * nt;
+#ifdef PMG_KTRACE
+            if (kslot == 1 && parity == 1 && threadIdx.x == 0 && blockIdx.x == 0) g_ktrace[0] = clock64();
+#endif
             warp_line_solve<true, KW>(y, C.cl + fo, C.cm + fo, nt, C.corner[(long)b * L.split + s]);
+#ifdef PMG_KTRACE
+            if (kslot == 1 && parity == 1 && threadIdx.x == 0 && blockIdx.x == 0) g_ktrace[1] = clock64();
+#endif
             __syncwarp();
 #pragma unroll
             for (int q = 0; q < KW; ++q)
                 if (q < KE && j0 + q < nt) U[s * nt + j0 + q] = y[q];
         }
         team.sync();
+        KTS(kslot, 1 + parity);
     }
     if (L.len <= 0) return;
     const int n = L.n;
@@ -2102,6 +2120,7 @@ __device__ void coarse_smooth(const CoarseLevel& C, int b, const Team& team) {
                 if (q < KE && j0 + q < L.len) U[base + j0 + q] = y[q];
         }
         team.sync();
+        KTS(kslot, 3 + parity);
     }
 }
 
@@ -2268,7 +2287,12 @@ __device__ void tail_body(const CoarseParams& cp, const int* __restrict__ prog, 
     const BlockTeam team;
     for (int i = 0; i < nops; ++i) {
         const int op = prog[i] & 255, l = prog[i] >> 8;
-        exec_op<KW, false>(op, lv[l], lv[l + (op == OP_COARSE ? 0 : 1)], simg.env, 0, team);
+        // level descriptors copied into registers: the shared-memory vectors
+        // the phase stores to could alias the shared table, which would force
+        // a reload of every field after every store
+        const CoarseLevel Cl = lv[l], Dl = lv[l + (op == OP_COARSE ? 0 : 1)];
+        const EnvFactor env = simg.env;
+        exec_op<KW, false>(op, Cl, Dl, env, 0, team);
         __syncthreads();
         if (trace && threadIdx.x == 0) trace[2 + i] = globaltimer();
     }
@@ -2813,7 +2837,7 @@ void launch_flush(double* buf, long n, cudaStream_t st) {
 
 namespace pmg {
 #ifdef PMG_KTRACE
-void read_ktrace(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_ktrace, sizeof(g_ktrace)); }
+void read_ktrace(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_ktrace, sizeof(g_ktrace)); }  // 32 entries
 #endif
 
 void launch_mid_cycle(const MidParams& mp, const int* prog, int nops, int B, const int* active,
