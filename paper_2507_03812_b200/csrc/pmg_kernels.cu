@@ -1463,9 +1463,16 @@ __global__ void __launch_bounds__(256, PMG_CL_MINB) k_radial_cl(LevelView L, dou
     double* Mx = IL + pn;
     double* scr = Mx + pn;
     const long fo = ((long)b * L.nt + t) * len;
-    for (int j = threadIdx.x; j < nloc; j += T) IL[P(j)] = __drcp_rn(ril[fo + row0 + j]);
-    for (int j = threadIdx.x; j <= nloc; j += T)
-        Mx[P(j)] = row0 + j > 0 ? rm[fo + row0 + j - 1] : 0.0;
+    // line factors: asynchronous copies overlapped with the rhs gather
+    for (int j = threadIdx.x; j < nloc; j += T)
+        __pipeline_memcpy_async(&IL[P(j)], &ril[fo + row0 + j], 8);
+    for (int j = threadIdx.x; j <= nloc; j += T) {
+        if (row0 + j > 0)
+            __pipeline_memcpy_async(&Mx[P(j)], &rm[fo + row0 + j - 1], 8);
+        else
+            Mx[P(j)] = 0.0;
+    }
+    __pipeline_commit();
     const int tm = L.tminus(t), tp = L.tplus(t);
     const double km = L.k[tm], kp = L.k[t], rkm = L.rk[tm], rkp = L.rk[t];
     const int dTM = (tm - t) * len, dTP = (tp - t) * len;
@@ -1517,6 +1524,8 @@ __global__ void __launch_bounds__(256, PMG_CL_MINB) k_radial_cl(LevelView L, dou
         }
         Y[P(j)] = acc;
     }
+    __pipeline_wait_prior(0);
+    for (int j = threadIdx.x; j < nloc; j += T) IL[P(j)] = __drcp_rn(IL[P(j)]);
     __syncthreads();
     line_solve_cl<K, false>(Y, IL, Mx, nloc, row0, len, 0.0, scr, xch);
     for (int j = threadIdx.x; j < nloc; j += T) U[base + row0 + j] = Y[P(j)];
@@ -1556,9 +1565,16 @@ __global__ void __launch_bounds__(256, PMG_CL_MINB) k_circle_cl(LevelView L, dou
     double* Mx = IL + pn;
     double* scr = Mx + pn;
     const long fo = (long)b * L.split * nt + (long)s * nt;
-    for (int j = threadIdx.x; j < nloc; j += T) IL[P(j)] = __drcp_rn(cil[fo + row0 + j]);
-    for (int j = threadIdx.x; j <= nloc; j += T)
-        Mx[P(j)] = row0 + j > 0 ? cm[fo + row0 + j - 1] : 0.0;
+    // line factors: asynchronous copies overlapped with the rhs gather
+    for (int j = threadIdx.x; j < nloc; j += T)
+        __pipeline_memcpy_async(&IL[P(j)], &cil[fo + row0 + j], 8);
+    for (int j = threadIdx.x; j <= nloc; j += T) {
+        if (row0 + j > 0)
+            __pipeline_memcpy_async(&Mx[P(j)], &cm[fo + row0 + j - 1], 8);
+        else
+            Mx[P(j)] = 0.0;
+    }
+    __pipeline_commit();
     const CoefAt<ONFLY> cf{&L, off, b};
     for (int j = threadIdx.x; j < nloc; j += T) {
         const int t = row0 + j, p = base + t;
@@ -1577,6 +1593,8 @@ __global__ void __launch_bounds__(256, PMG_CL_MINB) k_circle_cl(LevelView L, dou
         }
         Y[P(j)] = acc;
     }
+    __pipeline_wait_prior(0);
+    for (int j = threadIdx.x; j < nloc; j += T) IL[P(j)] = __drcp_rn(IL[P(j)]);
     __syncthreads();
     line_solve_cl<K, true>(Y, IL, Mx, nloc, row0, nt, corner[(long)b * L.split + s], scr, xch);
     for (int j = threadIdx.x; j < nloc; j += T) U[base + row0 + j] = Y[P(j)];
