@@ -888,7 +888,65 @@ __global__ void __launch_bounds__(256, 4) k_apply_tiled(LevelView L, TileGeom G,
     // neighbour strides in the tile: radial (s+-1) and angular (t+-1)
     const int dS = circ ? kTW : 1, dT = circ ? 1 : kTW;
     const int kk = threadIdx.x & (kTR - 1);
+    // interior tile: every row of it and of its halo lines is a non-Dirichlet
+    // ring away from the origin, so the row takes the lean form below (the
+    // row_from expressions with has_sm = has_sp = true, no phantom)
+    const bool lean = circ ? (slow0 >= 2 && slow0 + kTS + 1 <= min(split, N))
+                           : (fast0 >= 1 && split + fast0 >= 2 && fast0 + kTR + 2 <= len);
     double v = 0.0;
+    if (lean) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int jj = (threadIdx.x >> 6) + 4 * q;
+            int s, t;
+            bool mine;
+            if (circ) {
+                s = slow0 + jj;
+                t = fast0 + kk;
+                mine = t < nt;
+            } else {
+                t = slow0 + jj;
+                s = split + fast0 + kk;
+                mine = t < nt;
+            }
+            double val = 0.0;
+            if (mine) {
+                const int e = (jj + 1) * kTW + (kk + 1);
+                const int tm = t == 0 ? nt - 1 : t - 1;
+                const double km = L.k[tm], kp = L.k[t];
+                const double hm = L.h[s - 1], hp = L.h[s];
+                const double kbar = 0.5 * (km + kp);
+                const double hbar = 0.5 * (hm + hp);
+                const double qkm = xdiv(kbar, hm, L.rh[s - 1]);
+                const double qkp = xdiv(kbar, hp, L.rh[s]);
+                const double qhm = xdiv(hbar, km, L.rk[tm]);
+                const double qhp = xdiv(hbar, kp, L.rk[t]);
+                const double aP = sArr[e], aSM = sArr[e - dS], aSP = sArr[e + dS];
+                const double tP = sAtt[e], tTM = sAtt[e - dT], tTP = sAtt[e + dT];
+                const double rTM = sArt[e - dT], rTP = sArt[e + dT];
+                const double rSM = sArt[e - dS], rSP = sArt[e + dS];
+                double diag = 0.0;
+                diag += qkm * (aP + aSM);
+                diag += qkp * (aP + aSP);
+                diag += qhm * (tP + tTM);
+                diag += qhp * (tP + tTP);
+                diag += L.beta[(long)b * L.nr + s] * sDet[e] * hbar * kbar;
+                double acc = 0.0;
+                acc += diag * sU[e];
+                acc += (-qkm * (aP + aSM)) * sU[e - dS];
+                acc += (-qkp * (aP + aSP)) * sU[e + dS];
+                acc += (-qhm * (tP + tTM)) * sU[e - dT];
+                acc += (-qhp * (tP + tTP)) * sU[e + dT];
+                acc += (-(rTM + rSM) * 0.25) * sU[e - dS - dT];
+                acc += ((rSM + rTP) * 0.25) * sU[e - dS + dT];
+                acc += ((rTM + rSP) * 0.25) * sU[e + dS - dT];
+                acc += (-(rSP + rTP) * 0.25) * sU[e + dS + dT];
+                val = MODE == 0 ? acc : sF[jj * kTR + kk] - acc;
+                out[off + (circ ? s * nt + t : split * nt + t * len + (s - split))] = val;
+            }
+            if (NORM) v = norm_type == 2 ? fmax(v, fabs(val)) : v + val * val;
+        }
+    } else
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
         const int jj = (threadIdx.x >> 6) + 4 * q;
@@ -2513,9 +2571,13 @@ void set_smem(KernelT kern, size_t bytes) {
 // chunk size K and threads T for a line of n rows: T = 32*ceil(ceil(n/K)/32) <= 512
 inline void line_shape(int n, int& K, int& T) {
     static const int ks[4] = {2, 4, 8, 16};
+    static const int maxt = [] {
+        const char* e = std::getenv("PMG_LINE_MAXT");
+        return e ? std::atoi(e) : 256;
+    }();
     K = 16;
     for (int q = 0; q < 4; ++q)
-        if ((n + ks[q] - 1) / ks[q] <= 256 || ks[q] == 16) {
+        if ((n + ks[q] - 1) / ks[q] <= maxt || ks[q] == 16) {
             K = ks[q];
             break;
         }
