@@ -642,6 +642,42 @@ __device__ void origin_solve_serial(double* Y, double* X, const OriginFactor& of
     for (int k = 0; k < n; ++k) Y[P((k & 1) ? h + (k >> 1) : (k >> 1))] = X[k];
 }
 
+// Circle-line rhs (smoother.cpp:162-182) of an interior Take ring: rings
+// s-1, s+1 are circle rings and not Dirichlet, so the off-line couplings are
+// the row_from expressions with has_sm = has_sp = true (same values).
+__device__ __forceinline__ bool circle_lean_ring(const LevelView& L, int s) {
+#ifdef PMG_NO_CIRCLE_LEAN
+    return false;
+#endif
+    return s >= 1 && s + 1 < L.split && s + 1 < L.nr - 1 && !(s == 1 && L.boundary == 1);
+}
+__device__ __forceinline__ double circle_rhs_lean(const LevelView& L, long off, int s, int t,
+                                                  const double* __restrict__ U,
+                                                  const double* __restrict__ F) {
+    const int nt = L.nt, p = s * nt + t;
+    const int tm = t == 0 ? nt - 1 : t - 1, tp = t + 1 == nt ? 0 : t + 1;
+    const int pTM = s * nt + tm, pTP = s * nt + tp;
+    const double* A = L.arr + off;
+    const double* R = L.art + off;
+    const double aP = A[p], aSM = A[p - nt], aSP = A[p + nt];
+    const double rTM = R[pTM], rTP = R[pTP], rSM = R[p - nt], rSP = R[p + nt];
+    const double uSM = U[p - nt], uSP = U[p + nt];
+    const double uSMTM = U[pTM - nt], uSMTP = U[pTP - nt];
+    const double uSPTM = U[pTM + nt], uSPTP = U[pTP + nt];
+    const double fP = F[p];
+    const double kbar = 0.5 * (L.k[tm] + L.k[t]);
+    const double qkm = xdiv(kbar, L.h[s - 1], L.rh[s - 1]);
+    const double qkp = xdiv(kbar, L.h[s], L.rh[s]);
+    double acc = fP;
+    acc -= (-qkm * (aP + aSM)) * uSM;
+    acc -= (-qkp * (aP + aSP)) * uSP;
+    acc -= (-(rTM + rSM) * 0.25) * uSMTM;
+    acc -= ((rSM + rTP) * 0.25) * uSMTP;
+    acc -= ((rTM + rSP) * 0.25) * uSPTM;
+    acc -= (-(rSP + rTP) * 0.25) * uSPTP;
+    return acc;
+}
+
 // ------------------------------------------------------------ apply / residual
 // y = A u or r = f - A u with the Take/Give row of stencil.cpp:44-137 and the
 // accumulation order of apply_take (stencil.cpp:166-171).
@@ -1082,6 +1118,8 @@ __global__ void __launch_bounds__(512) k_circle(LevelView L, double* __restrict_
             acc -= Rw[8 * n + p] * U[q.pSPTP];
             Y[P(t)] = acc;
         }
+    } else if (!ONFLY && circle_lean_ring(L, s)) {
+        for (int t = threadIdx.x; t < nt; t += T) Y[P(t)] = circle_rhs_lean(L, off, s, t, U, F);
     } else
     for (int t = threadIdx.x; t < nt; t += T) {
         const int p = base + t;
@@ -1634,6 +1672,11 @@ __global__ void __launch_bounds__(256, PMG_CL_MINB) k_circle_cl(LevelView L, dou
     }
     __pipeline_commit();
     const CoefAt<ONFLY> cf{&L, off, b};
+    const bool lean = !ONFLY && circle_lean_ring(L, s);
+    if (lean)
+        for (int j = threadIdx.x; j < nloc; j += T)
+            Y[P(j)] = circle_rhs_lean(L, off, s, row0 + j, U, F);
+    else
     for (int j = threadIdx.x; j < nloc; j += T) {
         const int t = row0 + j, p = base + t;
         const Nbr q = neighbours(L, s, t, p);
