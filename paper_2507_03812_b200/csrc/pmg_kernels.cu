@@ -361,36 +361,56 @@ __device__ void origin_solve(double* Y, double* X, const OriginFactor& of, int b
     const int j0 = threadIdx.x * K;
     for (int k = threadIdx.x; k < n; k += T) X[P(k)] = Y[P((k & 1) ? h + (k >> 1) : (k >> 1))];
     __syncthreads();
+    KT(6);
+    // the thread's factor entries are loaded up front (independent loads in
+    // flight together), not inside the sequential compose chains
+    double b1v[K + 1], b2v[K + 2];
+#pragma unroll
+    for (int q = 0; q < K + 2; ++q) {
+        const int i = j0 + q;
+        if (q < K + 1) b1v[q] = (i >= 1 && i < nb) ? b1[i] : 0.0;
+        b2v[q] = (i >= 2 && i < nb) ? b2[i] : 0.0;
+    }
     // forward band: z_i = x_i - L(i,i-2) z_{i-2} - L(i,i-1) z_{i-1}; state (z_{i-1}, z_i)
     Map2 m = {1.0, 0.0, 0.0, 1.0, 0.0, 0.0};
 #pragma unroll
     for (int q = 0; q < K; ++q) {
         const int i = j0 + q;
         if (i < nb) {
-            const double l1 = i >= 1 ? b1[i] : 0.0, l2 = i >= 2 ? b2[i] : 0.0;
-            const Map2 mi = {0.0, 1.0, -l2, -l1, 0.0, X[P(i)]};
+            const Map2 mi = {0.0, 1.0, -b2v[q], -b1v[q], 0.0, X[P(i)]};
             m = compose2(mi, m);
         }
     }
     double zm2, zm1;
+    KT(7);
     block_scan2<true>(m, zm2, zm1, scr);
+    KT(8);
+    double r1v[K], r2v[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+        const int i = j0 + q;
+        r1v[q] = (i < nb && i >= of.fc1) ? r1[i] : 0.0;
+        r2v[q] = (i < nb && i >= of.fc2) ? r2[i] : 0.0;
+    }
     double s1 = 0.0, s2 = 0.0;
 #pragma unroll
     for (int q = 0; q < K; ++q) {
         const int i = j0 + q;
         if (i < nb) {
             double sum = X[P(i)];
-            if (i >= 2) sum -= b2[i] * zm2;
-            if (i >= 1) sum -= b1[i] * zm1;
+            if (i >= 2) sum -= b2v[q] * zm2;
+            if (i >= 1) sum -= b1v[q] * zm1;
             X[P(i)] = sum;
             zm2 = zm1;
             zm1 = sum;
-            if (i >= of.fc1) s1 += r1[i] * sum;
-            if (i >= of.fc2) s2 += r2[i] * sum;
+            if (i >= of.fc1) s1 += r1v[q] * sum;
+            if (i >= of.fc2) s2 += r2v[q] * sum;
         }
     }
+    KT(9);
     s1 = block_sum(s1, scr);
     s2 = block_sum(s2, scr + 32);
+    KT(10);
     if (threadIdx.x == 0) {  // dense closing rows, then their diagonal scaling
         const double zn2 = X[P(n - 2)] - s1;
         double zn1 = X[P(n - 1)] - s2;
@@ -402,41 +422,49 @@ __device__ void origin_solve(double* Y, double* X, const OriginFactor& of, int b
         X[P(n - 2)] = xn2;
     }
     __syncthreads();
+    KT(11);
     const double xn1 = X[P(n - 1)], xn2 = X[P(n - 2)];
     // backward band: x_k = g_k - L(k+2,k) x_{k+2} - L(k+1,k) x_{k+1},
     // g_k = w_k - L(n-1,k) x_{n-1} - L(n-2,k) x_{n-2}; state (x_{k+1}, x_{k+2})
+    double dv[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) dv[q] = j0 + q < nb ? D[j0 + q] : 1.0;
     Map2 g = {1.0, 0.0, 0.0, 1.0, 0.0, 0.0};
 #pragma unroll
     for (int q = K - 1; q >= 0; --q) {
         const int k = j0 + q;
         if (k < nb) {
-            double gk = X[P(k)] / D[k];
-            if (k >= of.fc2) gk -= r2[k] * xn1;
-            if (k >= of.fc1) gk -= r1[k] * xn2;
+            double gk = X[P(k)] / dv[q];
+            if (k >= of.fc2) gk -= r2v[q] * xn1;
+            if (k >= of.fc1) gk -= r1v[q] * xn2;
             X[P(k)] = gk;
-            const double l1 = k + 1 < nb ? b1[k + 1] : 0.0;
-            const double l2 = k + 2 < nb ? b2[k + 2] : 0.0;
+            const double l1 = k + 1 < nb ? b1v[q + 1] : 0.0;
+            const double l2 = k + 2 < nb ? b2v[q + 2] : 0.0;
             const Map2 mk = {-l1, -l2, 1.0, 0.0, gk, 0.0};
             g = compose2(mk, g);
         }
     }
     double xp1, xp2;
+    KT(12);
     block_scan2<false>(g, xp1, xp2, scr);
+    KT(13);
 #pragma unroll
     for (int q = K - 1; q >= 0; --q) {
         const int k = j0 + q;
         if (k < nb) {
             double x = X[P(k)];
-            if (k + 2 < nb) x -= b2[k + 2] * xp2;
-            if (k + 1 < nb) x -= b1[k + 1] * xp1;
+            if (k + 2 < nb) x -= b2v[q + 2] * xp2;
+            if (k + 1 < nb) x -= b1v[q + 1] * xp1;
             X[P(k)] = x;
             xp2 = xp1;
             xp1 = x;
         }
     }
     __syncthreads();
+    KT(14);
     for (int k = threadIdx.x; k < n; k += T) Y[P((k & 1) ? h + (k >> 1) : (k >> 1))] = X[P(k)];
     __syncthreads();
+    KT(15);
 }
 
 // Correctly rounded a / l given r = RN(1/l) (Markstein): q0 = RN(a r) is
@@ -2512,17 +2540,32 @@ __global__ void __launch_bounds__(256) k_norm_partials(const double* __restrict_
 }
 
 // compute_norm (multigrid.cpp:48-59) from block partials; one block per section
-__global__ void __launch_bounds__(256) k_norm_final(const double* __restrict__ partials,
-                                                    int nblk, long n, int norm_type,
-                                                    double* __restrict__ norms) {
+__global__ void __launch_bounds__(1024) k_norm_final(const double* __restrict__ partials,
+                                                     int nblk, long n, int norm_type,
+                                                     double* __restrict__ norms) {
     pdl_enter();
     const int b = blockIdx.x;
-    double a = 0.0;
-    for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
-        const double x = partials[(long)b * nblk + i];
-        a = norm_type == 2 ? fmax(a, x) : a + x;
+    const double* Pb = partials + (long)b * nblk;
+    // eight independent accumulators per thread so the loads overlap; fixed
+    // combination order (deterministic for a given launch shape)
+    double acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = 0.0;
+    const int T = blockDim.x;
+    for (int i0 = threadIdx.x; i0 < nblk; i0 += 8 * T) {
+        double x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int i = i0 + k * T;
+            x[k] = i < nblk ? Pb[i] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] = norm_type == 2 ? fmax(acc[k], x[k]) : acc[k] + x[k];
     }
-    __shared__ double red[8];
+    double a = acc[0];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) a = norm_type == 2 ? fmax(a, acc[k]) : a + acc[k];
+    __shared__ double red[32];
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
         const double o = __shfl_down_sync(FULL, a, d);
@@ -2932,7 +2975,8 @@ int launch_norm_partials(const double* v, long n, int B, int norm_type, double* 
 
 void launch_norm_final(const double* partials, int nblk, int B, long n, int norm_type,
                        double* norms, cudaStream_t st) {
-    launch_k(k_norm_final, B, 256, 0, st, partials, nblk, n, norm_type, norms);
+    launch_k(k_norm_final, B, nblk >= 4096 ? 1024 : 256, 0, st, partials, nblk, n, norm_type,
+             norms);
 }
 
 void launch_check(const double* norms, ConvState cs, int B, int max_it, double rel_tol,

@@ -15,6 +15,7 @@ import paper_2507_03812_b200 as pmg  # noqa: E402
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 level = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 kind = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+parity = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 geom, prob, grid, st, meta = pmg.baseline_config(k)
 s = pmg.MultigridSolver(geom, prob, grid, st)
 lib = C.CDLL(os.environ["PMG_LIB"])
@@ -23,9 +24,12 @@ n = s.n(level)
 u = np.random.default_rng(1).uniform(-1, 1, n)
 f = np.random.default_rng(2).uniform(-1, 1, n)
 for rep in range(5):
-    s.sweep(u, f, kind, 1, level)
+    s.sweep(u, f, kind, parity, level)
     lib.pmg_debug_ktrace(buf)
 marks = list(buf)
-d = [marks[i + 1] - marks[i] for i in range(6) if marks[i + 1] and marks[i]]
+d = [(i, marks[i + 1] - marks[i]) for i in range(6) if marks[i + 1] and marks[i]]
 print(f"level {level} kind {kind} shape {s.level_shape(level)}: phase cycles", d,
       "total", marks[5] - marks[0] if marks[5] else None)
+inner = [(i, marks[i + 1] - marks[i]) for i in range(6, 15) if marks[i + 1] and marks[i]]
+if inner:
+    print("  origin solve phases", inner)
