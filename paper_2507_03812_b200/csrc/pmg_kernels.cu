@@ -25,6 +25,12 @@ namespace pmg {
 
 namespace cg = cooperative_groups;
 
+// unroll of the single-CTA radial rhs gather (rows whose loads are in flight together)
+#ifndef PMG_RAD_UNROLL
+#define PMG_RAD_UNROLL 2
+#endif
+constexpr int kRadUnroll = PMG_RAD_UNROLL;
+
 #ifdef PMG_KTRACE
 // diagnostics build only: clock64 marks of thread 0 of block (0,0)
 __device__ unsigned long long g_ktrace[32];
@@ -1254,7 +1260,7 @@ __global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict_
         const double* __restrict__ ATT = L.att + off;
         const double* __restrict__ ART = L.art + off;
         const int N = L.nr - 1;
-#pragma unroll 2
+#pragma unroll (kRadUnroll)
         for (int i = ifirst + threadIdx.x; i <= ilast; i += T) {
             const int s = split + i, p = base + i;
             const double fP = F[p];
