@@ -1425,28 +1425,45 @@ __device__ __forceinline__ void cluster_carry(double At, const double (&Bt)[NV],
                                               double (&carry)[NV]) {
     cg::cluster_group cl = cg::this_cluster();
     const int rank = cl.block_rank(), C = cl.num_blocks();
+    // forward and backward passes use separate slots, so only the backward
+    // pass needs the trailing barrier (no CTA leaves while its slot is read)
+    double* slot = xch + (FWD ? 0 : 4);
     if (threadIdx.x == 0) {
-        xch[0] = At;
+        slot[0] = At;
 #pragma unroll
-        for (int v = 0; v < NV; ++v) xch[1 + v] = Bt[v];
+        for (int v = 0; v < NV; ++v) slot[1 + v] = Bt[v];
     }
     cl.sync();
+    // all remote slots loaded first (independent DSMEM loads in flight), then
+    // composed in rank order
+    double ra[8], rb[8][NV];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const bool use = FWD ? r < rank : (r > rank && r < C);
+        ra[r] = 1.0;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) rb[r][v] = 0.0;
+        if (use) {
+            const double* x = cl.map_shared_rank(slot, r);
+            ra[r] = x[0];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) rb[r][v] = x[1 + v];
+        }
+    }
 #pragma unroll
     for (int v = 0; v < NV; ++v) carry[v] = 0.0;
     if (FWD) {
-        for (int r = 0; r < rank; ++r) {
-            const double* x = cl.map_shared_rank(xch, r);
 #pragma unroll
-            for (int v = 0; v < NV; ++v) carry[v] = x[0] * carry[v] + x[1 + v];
-        }
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) carry[v] = ra[r] * carry[v] + rb[r][v];
     } else {
-        for (int r = C - 1; r > rank; --r) {
-            const double* x = cl.map_shared_rank(xch, r);
 #pragma unroll
-            for (int v = 0; v < NV; ++v) carry[v] = x[0] * carry[v] + x[1 + v];
-        }
+        for (int r = 7; r >= 0; --r)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) carry[v] = ra[r] * carry[v] + rb[r][v];
     }
-    cl.sync();  // remote reads done before the slots are reused
+    if (!FWD) cl.sync();  // remote reads done before any CTA of the cluster exits
 }
 
 // Solve of rows [row0, row0+nloc) of an ntot-row LL^T (+ SM) line held by a
