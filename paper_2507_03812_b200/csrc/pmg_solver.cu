@@ -258,7 +258,9 @@ struct Solver {
     template <class T>
     T* alloc(size_t count, bool zero = true) {
         void* p = nullptr;
-        const size_t nb = std::max<size_t>(count, 1) * sizeof(T);
+        // 64 bytes of tail padding: the bulk tile copies of k_apply_tiled read
+        // up to two elements past a line's last node
+        const size_t nb = std::max<size_t>(count, 1) * sizeof(T) + 64;
         PMG_CUDA(cudaMalloc(&p, nb));
         allocs.push_back(p);
         bytes += nb;
