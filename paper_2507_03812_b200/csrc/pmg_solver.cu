@@ -258,8 +258,8 @@ struct Solver {
     template <class T>
     T* alloc(size_t count, bool zero = true) {
         void* p = nullptr;
-        // 64 bytes of tail padding: the bulk tile copies of k_apply_tiled read
-        // up to two elements past a line's last node
+        // 64 bytes of tail padding: aligned bulk copies may round a segment's
+        // end up to the next 16-byte boundary
         const size_t nb = std::max<size_t>(count, 1) * sizeof(T) + 64;
         PMG_CUDA(cudaMalloc(&p, nb));
         allocs.push_back(p);
