@@ -2678,12 +2678,19 @@ void set_smem(KernelT kern, size_t bytes) {
 }
 
 // chunk size K and threads T for a line of n rows: T = 32*ceil(ceil(n/K)/32) <= 512
-inline void line_shape(int n, int& K, int& T) {
+// Threads per line: wide CTAs (short per-thread chunks) when few lines run
+// concurrently (latency), narrow CTAs when the batch of lines fills the GPU
+// many times over (throughput, e.g. 256 sections of config 3).
+inline void line_shape(int n, int& K, int& T, long lines_total = 0) {
     static const int ks[4] = {2, 4, 8, 16};
-    static const int maxt = [] {
+    static const int env_maxt = [] {
         const char* e = std::getenv("PMG_LINE_MAXT");
-        return e ? std::atoi(e) : 256;
+        return e ? std::atoi(e) : 0;
     }();
+    const int maxt = env_maxt > 0 ? env_maxt
+                     : lines_total >= 4096 ? 64
+                     : lines_total >= 2048 ? 128
+                                           : 256;
     K = 16;
     for (int q = 0; q < 4; ++q)
         if ((n + ks[q] - 1) / ks[q] <= maxt || ks[q] == 16) {
@@ -2900,7 +2907,7 @@ void launch_circle(const LevelView& L, bool onfly, double* u, const double* f, c
         }
         return;
     }
-    line_shape(L.nt, K, T);
+    line_shape(L.nt, K, T, (long)lines * L.B);
 #define PMG_C(KK)                                                                            \
     (onfly ? circle_k<true, KK>(L, u, f, cil, cm, corner, cz, of, parity, serial, exact_rings, \
                                 active, st, T, lines)                                      \
@@ -2955,7 +2962,7 @@ void launch_radial(const LevelView& L, bool onfly, double* u, const double* f, c
             launch_cluster(k_radial_cl<16>, C, grid, T, sm, st, L, u, f, ril, rm, parity, active);
         return;
     }
-    line_shape(L.len, K, T);
+    line_shape(L.len, K, T, (long)lines * L.B);
 #define PMG_R(KK)                                                                       \
     (onfly ? radial_k<true, KK>(L, u, f, ril, rm, parity, serial, active, st, T, lines) \
            : radial_k<false, KK>(L, u, f, ril, rm, parity, serial, active, st, T, lines))
