@@ -76,6 +76,39 @@ constexpr unsigned FULL = 0xffffffffu;
 #define PMG_ORIGIN_SCAN_MIN 0
 #endif
 
+// ------------------------------------------------ mbarrier + bulk copies (TMA engine)
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n\t"
+                 "fence.proxy.async.shared::cta;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// bulk global -> shared copy (TMA engine), completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
 __device__ __forceinline__ int P(int i) { return i + (i >> 4); }  // bank-conflict padding
 __host__ __device__ __forceinline__ int padded(int n) { return n + (n >> 4) + 1; }
 
@@ -1086,6 +1119,415 @@ __global__ void __launch_bounds__(256, 4) k_apply_tiled(LevelView L, TileGeom G,
             double a = red[0];
             for (int w = 1; w < 8; ++w) a = norm_type == 2 ? fmax(a, red[w]) : a + red[w];
             partials[(long)b * gridDim.x + blockIdx.x] = a;
+        }
+    }
+}
+
+// ------------------------------------------- TMA-streamed Take residual
+// A CTA owns a strip of kTW2 = 240 consecutive nodes along the contiguous
+// direction of a region (angles of a ring in the ring-major circle region;
+// rows of a spoke in the spoke-major radial region) and walks R lines across
+// it (rings, resp. spokes).  A producer warp streams each line -- u, arr, art,
+// att, det, f over the 242-node halo segment -- into a kLines-deep ring of
+// shared-memory slots with one bulk copy (TMA engine) per array and line,
+// completion counted on the slot's `full` mbarrier; the 8 consumer warps (30
+// output lanes + 2 halo lanes each) read each line once into a 3-line register
+// window, take in-line neighbours by warp shuffles, and release the slot on
+// its `empty` mbarrier.  HBM is read once per node; no per-element address
+// arithmetic and no block barriers in the loop.  Segments are copied from
+// their 16-byte-aligned start (node k of a line at slot position k + o, o the
+// parity of the line's first index).  The theta wrap of the circle strips at
+// both ends comes from two 16-byte edge copies per array.  Rings split-1 and
+// split (the region interface: their ring/spoke neighbours lie in the other
+// layout) are computed node-wise by extra CTAs of the same launch.
+// the lean interior row (k_apply_tiled's lean branch, same order)
+__device__ __forceinline__ double lean_row(double qkm, double qkp, double qhm, double qhp,
+                                           double bdhk, double aP, double aSM, double aSP,
+                                           double tP, double tTM, double tTP, double rTM,
+                                           double rTP, double rSM, double rSP, double uP,
+                                           double uSM, double uSP, double uTM, double uTP,
+                                           double uMM, double uMP, double uPM, double uPP) {
+    double diag = 0.0;
+    diag += qkm * (aP + aSM);
+    diag += qkp * (aP + aSP);
+    diag += qhm * (tP + tTM);
+    diag += qhp * (tP + tTP);
+    diag += bdhk;
+    double acc = 0.0;
+    acc += diag * uP;
+    acc += (-qkm * (aP + aSM)) * uSM;
+    acc += (-qkp * (aP + aSP)) * uSP;
+    acc += (-qhm * (tP + tTM)) * uTM;
+    acc += (-qhp * (tP + tTP)) * uTP;
+    acc += (-(rTM + rSM) * 0.25) * uMM;
+    acc += ((rSM + rTP) * 0.25) * uMP;
+    acc += ((rTM + rSP) * 0.25) * uPM;
+    acc += (-(rSP + rTP) * 0.25) * uPP;
+    return acc;
+}
+
+__device__ __forceinline__ bool lean_ring(const LevelView& L, int s) {
+    return s >= 1 && s <= L.nr - 3 && !(L.boundary == 1 && s == 1);
+}
+
+// general row (origin, Dirichlet, next-to-Dirichlet rings) from the window
+__device__ __noinline__ double general_row(const LevelView& L, int b, long off,
+                                              const double* __restrict__ u, int s, int t,
+                                              const Coef& cP, const Coef& cTM, const Coef& cTP,
+                                              const Coef& cSM, const Coef& cSP, double uP,
+                                              double uSM, double uSP, double uTM, double uTP,
+                                              double uMM, double uMP, double uPM, double uPP) {
+    if (L.dir(s)) return 1.0 * uP;
+    const int nt = L.nt;
+    const int tm = t == 0 ? nt - 1 : t - 1;
+    double anti = 0.0, uanti = 0.0;
+    if (s == 0 && L.boundary == 0) {  // phantom partner (0, t + nt/2)
+        const int t2 = t + nt / 2 >= nt ? t + nt / 2 - nt : t + nt / 2;
+        anti = L.arr[off + t2];
+        uanti = u[off + t2];
+    }
+    const Row R = row_from(L, b, s, t, tm, cP, cTM, cTP, cSM, cSP, anti);
+    double acc = 0.0;
+    acc += R.d * uP;
+    if (R.has_sm) acc += R.sm * uSM;
+    if (R.has_sp) acc += R.sp * uSP;
+    acc += R.tm * uTM;
+    acc += R.tp * uTP;
+    if (R.has_sm) {
+        acc += R.mm * uMM;
+        acc += R.mp * uMP;
+    }
+    if (R.has_sp) {
+        acc += R.pm * uPM;
+        acc += R.pp * uPP;
+    }
+    if (R.origin) acc += R.ph * uanti;
+    return acc;
+}
+
+constexpr int kTW2 = 240;             // output nodes per strip (8 warps x 30)
+constexpr int kLn = 248;              // slot row: 242 halo nodes + alignment slack
+#ifndef PMG_TMA_LINES
+#define PMG_TMA_LINES 5
+#endif
+#ifndef PMG_TMA_MINB
+#define PMG_TMA_MINB 2
+#endif
+constexpr int kLines = PMG_TMA_LINES;  // line slots per CTA
+struct TmaSlot {
+    double a[6][kLn];                 // u, arr, art, att, det, f
+    double e[2][5][2];                // circle theta-wrap edges (left, right)
+};
+constexpr size_t kTmaSmem = kLines * sizeof(TmaSlot) + 2 * kLines * 8 + 16;
+
+// Rows the strips compute are the lean interior rows: circle rings
+// c0 .. split-2 and radial rows s = split+1 .. N-2.  The rest -- origin /
+// interior-Dirichlet rings, the region interface rings split-1 and split, the
+// Dirichlet ring N and ring N-1 -- are computed node-wise by the last CTAs of
+// the launch.
+struct TmaGeom {
+    int c0;        // first strip ring (1, or 2 with an interior Dirichlet ring 0)
+    int ncf, ncs;  // circle strips: angle strips x ring chunks
+    int nrf, nrs;  // radial strips: row strips x spoke chunks
+    int nif;       // node-wise CTAs (256 nodes each)
+    int R;         // lines per strip
+    int cps;       // CTAs per section
+};
+
+inline TmaGeom tma_geom(const LevelView& L, int R) {
+    TmaGeom g;
+    g.R = R;
+    g.c0 = L.boundary == 1 ? 2 : 1;
+    const int cr = L.split - 1 - g.c0;  // rings c0 .. split-2
+    g.ncf = cr > 0 ? (L.nt + kTW2 - 1) / kTW2 : 0;
+    g.ncs = cr > 0 ? (cr + R - 1) / R : 0;
+    const int rr = L.len - 3;           // rows i = 1 .. len-3
+    g.nrf = rr > 0 ? (rr + kTW2 - 1) / kTW2 : 0;
+    g.nrs = rr > 0 ? (L.nt + R - 1) / R : 0;
+    g.nif = (6 * L.nt + 255) / 256;     // up to 6 node-wise rings
+    g.cps = g.ncf * g.ncs + g.nrf * g.nrs + g.nif;
+    return g;
+}
+
+inline TmaGeom tma_geom_auto(const LevelView& L) {
+    TmaGeom g = tma_geom(L, 64);
+    for (int R = 64; R > 8; R >>= 1) {
+        g = tma_geom(L, R);
+        if ((long)g.cps * L.B >= 148L * 4) break;
+    }
+    return g;
+}
+
+// whether the TMA kernel applies: long lines, even n_theta (16-byte aligned
+// ring starts), and enough nodes that bandwidth, not latency, bounds the launch
+// (latency-bound small levels keep the one-tile-per-CTA kernel)
+inline bool tma_ok(const LevelView& L) {
+    return L.nt >= 256 && (L.nt & 1) == 0 && L.len >= 64 && L.split >= 4 &&
+           (long)L.n * L.B >= (4L << 20);
+}
+
+// ring of node-wise row e (0 .. 6 nt): 0, 1, split-1, split, N-1, N; -1 when
+// that ring is a strip ring (or a duplicate)
+__device__ __forceinline__ int tma_nodewise_ring(const LevelView& L, int c0, int j) {
+    const int N = L.nr - 1;
+    switch (j) {
+        case 0: return 0;
+        case 1: return c0 == 2 ? 1 : -1;
+        case 2: return L.split - 1;
+        case 3: return L.split;
+        case 4: return N - 1 > L.split ? N - 1 : -1;
+        default: return N > L.split ? N : -1;
+    }
+}
+
+template <bool CIRC, int MODE, bool NORM>
+__device__ __forceinline__ double tma_strip(const LevelView& L, const TmaGeom& G, int b, int w,
+                                            const double* __restrict__ u,
+                                            const double* __restrict__ f,
+                                            double* __restrict__ out, int norm_type,
+                                            TmaSlot* slot, unsigned long long* full,
+                                            unsigned long long* empty) {
+    const int nt = L.nt, split = L.split, len = L.len;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long off = (long)b * L.n;
+    // strip: fast index of node k is f0 + k - 1; center lines l0 .. l1-1
+    int f0, l0, l1;
+    if (CIRC) {
+        f0 = (w % G.ncf) * kTW2;
+        l0 = G.c0 + (w / G.ncf) * G.R;
+        l1 = min(l0 + G.R, split - 1);
+    } else {
+        f0 = 1 + (w % G.nrf) * kTW2;
+        l0 = (w / G.nrf) * G.R;
+        l1 = min(l0 + G.R, nt);
+    }
+    const int nlines = l1 - l0 + 2;  // halo line l0-1, lines l0..l1-1, halo line l1
+    // global index of node k = 0 of line l (circle: ring l; radial: spoke l, wrapped)
+    auto line_base = [&](int l) -> long {
+        if (CIRC) return off + (long)l * nt + f0 - 1;
+        const int tt = l < 0 ? l + nt : (l >= nt ? l - nt : l);
+        return off + (long)split * nt + (long)tt * len + f0 - 1;
+    };
+    // last node of a line segment (circle: t <= nt-1; radial: row <= len-2)
+    const int khi = CIRC ? min(kTW2 + 1, nt - f0) : min(kTW2 + 1, len - 1 - f0);
+    const bool eL = CIRC && f0 == 0, eR = CIRC && f0 + kTW2 >= nt;
+    if (warp == 8) {
+        // ------------------------------------------------------ producer warp
+        auto src = [&](int a) -> const double* {
+            return a == 0 ? u : a == 1 ? L.arr : a == 2 ? L.art : a == 3 ? L.att : a == 4 ? L.det : f;
+        };
+        constexpr int narr = MODE == 1 ? 6 : 5;
+        for (int q = 0; q < nlines; ++q) {
+            const int sl = q % kLines;
+            if (q >= kLines) mbar_wait(&empty[sl], (unsigned)((q / kLines) - 1) & 1u);
+            const int l = l0 - 1 + q;
+            TmaSlot& S = slot[sl];
+            const long base = line_base(l);
+            const int o = (int)(base & 1);
+            const int p0 = ((eL ? 1 : 0) + o) & ~1;
+            const int p1 = (khi + o) | 1;
+            const long g0 = base + p0 - o;
+            const unsigned bytes = (unsigned)(p1 - p0 + 1) * 8u;
+            const unsigned ebytes = (eL ? 16u : 0u) + (eR ? 16u : 0u);
+            // the slot was last read through the generic proxy
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (lane == 0) mbar_arrive_tx(&full[sl], bytes * narr + ebytes * 5);
+            __syncwarp();
+            if (lane < narr) bulk_g2s(&S.a[lane][p0], src(lane) + g0, bytes, &full[sl]);
+            if (eL && lane >= 8 && lane < 13)  // t = nt-1 (odd index): the pair from nt-2
+                bulk_g2s(&S.e[0][lane - 8][0], src(lane - 8) + off + (long)l * nt + nt - 2, 16,
+                         &full[sl]);
+            if (eR && lane >= 16 && lane < 21)  // t = 0 of the ring
+                bulk_g2s(&S.e[1][lane - 16][0], src(lane - 16) + off + (long)l * nt, 16, &full[sl]);
+        }
+        return 0.0;
+    }
+    // ---------------------------------------------------------- consumer warps
+    const int k = warp * 30 + lane;  // node k of the segment
+    const int fi = f0 + k - 1;
+    const bool outl = lane >= 1 && lane <= 30 && (CIRC ? fi < nt : fi <= len - 3);
+    const bool useL = eL && k == 0;      // t = -1 -> nt-1
+    const bool useR = CIRC && fi == nt;  // t = nt -> 0
+    const int kc = min(k, kLn - 2);      // lanes past the segment read (unused) slot data
+    struct V {
+        double u, arr, art, att, det, f;
+    };
+    auto fetch = [&](int q) -> V {
+        V x;
+        const int sl = q % kLines;
+        mbar_wait(&full[sl], (unsigned)(q / kLines) & 1u);
+        const TmaSlot& S = slot[sl];
+        if (useL || useR) {
+            const int e = useL ? 0 : 1, i = useL ? 1 : 0;
+            x.u = S.e[e][0][i];
+            x.arr = S.e[e][1][i];
+            x.art = S.e[e][2][i];
+            x.att = S.e[e][3][i];
+            x.det = S.e[e][4][i];
+            x.f = 0.0;
+        } else {
+            const int pos = kc + (int)(line_base(l0 - 1 + q) & 1);
+            x.u = S.a[0][pos];
+            x.arr = S.a[1][pos];
+            x.art = S.a[2][pos];
+            x.att = S.a[3][pos];
+            x.det = S.a[4][pos];
+            x.f = MODE == 1 ? S.a[5][pos] : 0.0;
+        }
+        __syncwarp();
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[sl]))
+                         : "memory");
+        return x;
+    };
+    // per-lane constants along the strip
+    double km = 0, kp = 0, rkm = 0, rkp = 0, kbar = 0;
+    double hm = 0, hp = 0, rhm = 0, rhp = 0, hbar = 0, beta = 0;
+    int t = 0;
+    if (CIRC) {
+        t = fi < 0 ? fi + nt : (fi >= nt ? fi - nt : fi);
+        const int tm = t == 0 ? nt - 1 : t - 1;
+        km = L.k[tm];
+        kp = L.k[t];
+        rkm = L.rk[tm];
+        rkp = L.rk[t];
+        kbar = 0.5 * (km + kp);
+    } else {
+        const int s = split + max(1, min(fi, len - 3));
+        hm = L.h[s - 1];
+        hp = L.h[s];
+        rhm = L.rh[s - 1];
+        rhp = L.rh[s];
+        hbar = 0.5 * (hm + hp);
+        beta = L.beta[(long)b * L.nr + s];
+    }
+    V M = fetch(0), C = fetch(1);
+    double v = 0.0;
+    for (int q = 2; q < nlines; ++q) {
+        const V P = fetch(q);
+        const int l = l0 + q - 2;  // center line
+        double val = 0.0;
+        if (CIRC) {
+            const double uTM = __shfl_up_sync(FULL, C.u, 1), uTP = __shfl_down_sync(FULL, C.u, 1);
+            const double uMM = __shfl_up_sync(FULL, M.u, 1), uMP = __shfl_down_sync(FULL, M.u, 1);
+            const double uPM = __shfl_up_sync(FULL, P.u, 1), uPP = __shfl_down_sync(FULL, P.u, 1);
+            const double tTM = __shfl_up_sync(FULL, C.att, 1), tTP = __shfl_down_sync(FULL, C.att, 1);
+            const double rTM = __shfl_up_sync(FULL, C.art, 1), rTP = __shfl_down_sync(FULL, C.art, 1);
+            if (outl) {
+                const int s = l;
+                const double hm2 = L.h[s - 1], hp2 = L.h[s];
+                const double hb = 0.5 * (hm2 + hp2);
+                const double qkm = xdiv(kbar, hm2, L.rh[s - 1]);
+                const double qkp = xdiv(kbar, hp2, L.rh[s]);
+                const double qhm = xdiv(hb, km, rkm);
+                const double qhp = xdiv(hb, kp, rkp);
+                const double acc =
+                    lean_row(qkm, qkp, qhm, qhp, L.beta[(long)b * L.nr + s] * C.det * hb * kbar,
+                             C.arr, M.arr, P.arr, C.att, tTM, tTP, rTM, rTP, M.art, P.art, C.u,
+                             M.u, P.u, uTM, uTP, uMM, uMP, uPM, uPP);
+                val = MODE == 0 ? acc : C.f - acc;
+                out[off + (long)s * nt + t] = val;
+            }
+        } else {
+            const double uSM = __shfl_up_sync(FULL, C.u, 1), uSP = __shfl_down_sync(FULL, C.u, 1);
+            const double uMM = __shfl_up_sync(FULL, M.u, 1), uPM = __shfl_down_sync(FULL, M.u, 1);
+            const double uMP = __shfl_up_sync(FULL, P.u, 1), uPP = __shfl_down_sync(FULL, P.u, 1);
+            const double aSM = __shfl_up_sync(FULL, C.arr, 1), aSP = __shfl_down_sync(FULL, C.arr, 1);
+            const double rSM = __shfl_up_sync(FULL, C.art, 1), rSP = __shfl_down_sync(FULL, C.art, 1);
+            if (outl) {
+                const int tc = l;
+                const int tm = tc == 0 ? nt - 1 : tc - 1;
+                const double km2 = L.k[tm], kp2 = L.k[tc];
+                const double kb = 0.5 * (km2 + kp2);
+                const double qkm = xdiv(kb, hm, rhm);
+                const double qkp = xdiv(kb, hp, rhp);
+                const double qhm = xdiv(hbar, km2, L.rk[tm]);
+                const double qhp = xdiv(hbar, kp2, L.rk[tc]);
+                const double acc =
+                    lean_row(qkm, qkp, qhm, qhp, beta * C.det * hbar * kb, C.arr, aSM, aSP, C.att,
+                             M.att, P.att, M.art, P.art, rSM, rSP, C.u, uSM, uSP, M.u, P.u, uMM,
+                             uMP, uPM, uPP);
+                val = MODE == 0 ? acc : C.f - acc;
+                out[off + (long)split * nt + (long)tc * len + fi] = val;
+            }
+        }
+        if (NORM) v = norm_type == 2 ? fmax(v, fabs(val)) : v + val * val;
+        M = C;
+        C = P;
+    }
+    return v;
+}
+
+template <int MODE, bool NORM>
+__global__ void __launch_bounds__(288, PMG_TMA_MINB) k_apply_tma(LevelView L, TmaGeom G,
+                                                      const double* __restrict__ u,
+                                                      const double* __restrict__ f,
+                                                      double* __restrict__ out,
+                                                      double* __restrict__ partials, int norm_type,
+                                                      const int* __restrict__ active) {
+    pdl_enter();
+    extern __shared__ __align__(128) unsigned char tsm[];
+    __shared__ double red[9];
+    const int b = blockIdx.x / G.cps;
+    if (active && !active[b]) return;
+    const int w = blockIdx.x - b * G.cps;
+    const int nc = G.ncf * G.ncs, nrad = G.nrf * G.nrs;
+    double v = 0.0;
+    if (w < nc + nrad) {
+        TmaSlot* slot = reinterpret_cast<TmaSlot*>(tsm);
+        unsigned long long* full =
+            reinterpret_cast<unsigned long long*>(tsm + kLines * sizeof(TmaSlot));
+        unsigned long long* empty = full + kLines;
+        if (threadIdx.x == 0)
+            for (int i = 0; i < kLines; ++i) {
+                mbar_init(&full[i], 1);
+                mbar_init(&empty[i], 8);
+            }
+        __syncthreads();
+        if (w < nc)
+            v = tma_strip<true, MODE, NORM>(L, G, b, w, u, f, out, norm_type, slot, full, empty);
+        else
+            v = tma_strip<false, MODE, NORM>(L, G, b, w - nc, u, f, out, norm_type, slot, full,
+                                             empty);
+    } else if (threadIdx.x < 256) {
+        // node-wise rings (origin, interior Dirichlet, region interface, N-1, N)
+        const int e = (w - nc - nrad) * 256 + threadIdx.x;
+        const int s = e < 6 * L.nt ? tma_nodewise_ring(L, G.c0, e / L.nt) : -1;
+        if (s >= 0) {
+            const int t = e % L.nt;
+            const long off = (long)b * L.n;
+            const double* U = u + off;
+            const int p = L.idx(s, t);
+            const Nbr q = neighbours(L, s, t, p);
+            const CoefAt<false> cf{&L, off, b};
+            const int N = L.nr - 1;
+            const Coef z = {0.0, 0.0, 0.0, 0.0};
+            const Coef cP = cf(s, t, p), cTM = cf(s, q.tm, q.pTM), cTP = cf(s, q.tp, q.pTP);
+            const Coef cSM = s > 0 ? cf(s - 1, t, q.pSM) : z;
+            const Coef cSP = s < N ? cf(s + 1, t, q.pSP) : z;
+            const double uSM = s > 0 ? U[q.pSM] : 0.0, uSP = s < N ? U[q.pSP] : 0.0;
+            const double uMM = s > 0 ? U[q.pSMTM] : 0.0, uMP = s > 0 ? U[q.pSMTP] : 0.0;
+            const double uPM = s < N ? U[q.pSPTM] : 0.0, uPP = s < N ? U[q.pSPTP] : 0.0;
+            const double acc = general_row(L, b, off, u, s, t, cP, cTM, cTP, cSM, cSP, U[p], uSM,
+                                           uSP, U[q.pTM], U[q.pTP], uMM, uMP, uPM, uPP);
+            const double val = MODE == 0 ? acc : f[off + p] - acc;
+            out[off + p] = val;
+            if (NORM) v = norm_type == 2 ? fabs(val) : val * val;
+        }
+    }
+    if (NORM) {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            const double o = __shfl_down_sync(FULL, v, d);
+            v = norm_type == 2 ? fmax(v, o) : v + o;
+        }
+        if (lane == 0) red[warp] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double a = red[0];
+            for (int k2 = 1; k2 < 9; ++k2) a = norm_type == 2 ? fmax(a, red[k2]) : a + red[k2];
+            partials[blockIdx.x] = a;
         }
     }
 }
@@ -2294,38 +2736,6 @@ __device__ void coarse_smooth(const CoarseLevel& C, int b, const Team& team) {
     }
 }
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n\t"
-                 "fence.proxy.async.shared::cta;" ::"r"(smem_u32(bar)), "r"(count)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// bulk global -> shared copy (TMA engine), completion counted on `bar`
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
-                                         unsigned long long* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -2733,7 +3143,21 @@ static void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 
 int apply_launches(const LevelView& L) { return 1; }
 
-int apply_blocks(const LevelView& L) { return tile_geom(L).ntiles(); }
+
+
+int apply_blocks(const LevelView& L) {
+    return std::max(tile_geom(L).ntiles(), tma_geom_auto(L).cps);
+}
+
+// Take residual/apply through the TMA-streamed kernel (PMG_TMA_APPLY=0: off)
+static bool tma_apply_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("PMG_TMA_APPLY");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    return on;
+}
+
 
 int launch_apply(const LevelView& L, bool onfly, int mode, const double* u, const double* f,
                  double* out, double* partials, int norm_type, const int* active,
@@ -2742,10 +3166,26 @@ int launch_apply(const LevelView& L, bool onfly, int mode, const double* u, cons
         launch_k(k_residual_rows, dim3((L.n + 255) / 256, L.B), 256, 0, st, L, u, f, out, active);
         return 0;
     }
+    const bool norm = partials != nullptr;
+    if (!onfly && tma_apply_on() && tma_ok(L)) {
+        const TmaGeom S = tma_geom_auto(L);
+#define PMG_TMA(MO, NO)                                                                     \
+    do {                                                                                    \
+        set_smem(k_apply_tma<MO, NO>, kTmaSmem);                                            \
+        launch_k(k_apply_tma<MO, NO>, dim3(S.cps * L.B), 288, kTmaSmem, st, L, S, u, f, out, \
+                 partials, norm_type, active);                                              \
+    } while (0)
+        if (mode == 0) {
+            if (norm) PMG_TMA(0, true); else PMG_TMA(0, false);
+        } else {
+            if (norm) PMG_TMA(1, true); else PMG_TMA(1, false);
+        }
+#undef PMG_TMA
+        return S.cps;
+    }
     const TileGeom G = tile_geom(L);
     const int nb = G.ntiles();
     dim3 grid(nb, L.B);
-    const bool norm = partials != nullptr;
 #define PMG_APPLY(ON, MO, NO) \
     launch_k(k_apply_tiled<ON, MO, NO>, grid, 256, 0, st, L, G, u, f, out, partials, norm_type, active)
     if (onfly) {
