@@ -1860,24 +1860,113 @@ __device__ __forceinline__ void block_scan_ex(double A, double (&B)[NV], double&
     __syncthreads();
 }
 
-// Carry entering this CTA: the CTA totals of the earlier ranks (scan order)
-// composed and applied to 0.  xch: this CTA's NV+1 exchange slots.
+// Cluster exchange of the line solves without cluster barriers: each CTA
+// pushes its chunk total into a slot of every CTA that needs it with st.async
+// (DSMEM store whose bytes complete a transaction count on the destination's
+// mbarrier) and waits only on its own mbarrier for the totals it needs (the
+// earlier ranks forward, the later ranks backward, the two end rows for the
+// Sherman-Morrison correction).  Every CTA receives everything it waits for
+// before it exits, so no CTA is written after exit.  (A cluster barrier
+// compiles to a GPU-scope MEMBAR plus an L1 invalidate; three of them per line
+// were the largest stall of the clustered line kernels.)
+struct ClX {
+    double slot[2][8][4];         // [forward/backward][rank] = A, B0, B1
+    double ends[4];               // x0, z0, x_last, z_last
+    unsigned long long bar[3];    // forward, backward, ends
+};
+__device__ __forceinline__ unsigned mapa(const void* p, int rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async2(unsigned raddr, double a, double b, unsigned rbar) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+        "d"(a), "d"(b), "r"(rbar)
+        : "memory");
+}
+__device__ __forceinline__ void st_async1(unsigned raddr, double a, unsigned rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr),
+                 "d"(a), "r"(rbar)
+                 : "memory");
+}
+// At kernel start (all threads): barriers armed with the bytes this CTA will
+// receive, then a cluster arrive; clx_ready() (the matching wait) must run
+// before the first push -- call it after the rhs gather so its latency hides.
+template <int NV, bool CYC>
+__device__ __forceinline__ void clx_init(ClX& x) {
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = cl.block_rank(), C = cl.num_blocks();
+    constexpr unsigned push = NV == 1 ? 16u : 24u;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 3; ++i)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&x.bar[i])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // the single pending arrival gates each phase, so bytes may land
+        // before their expect-tx (the tx-count may go transiently negative)
+        mbar_arrive_tx(&x.bar[0], push * rank);
+        mbar_arrive_tx(&x.bar[1], push * (C - 1 - rank));
+        if (CYC) mbar_arrive_tx(&x.bar[2], 16u * ((rank != 0) + (rank != C - 1)));
+    }
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void clx_ready() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 template <int NV, bool FWD>
-__device__ __forceinline__ void cluster_carry(double At, const double (&Bt)[NV], double* xch,
+__device__ __forceinline__ void cluster_carry(double At, const double (&Bt)[NV], ClX& x,
                                               double (&carry)[NV]) {
     cg::cluster_group cl = cg::this_cluster();
     const int rank = cl.block_rank(), C = cl.num_blocks();
-    // forward and backward passes use separate slots, so only the backward
-    // pass needs the trailing barrier (no CTA leaves while its slot is read)
-    double* slot = xch + (FWD ? 0 : 4);
+    const int bank = FWD ? 0 : 1;
+    const int q = threadIdx.x;
+    if (q < C && (FWD ? q > rank : q < rank)) {
+        const unsigned ra = mapa(&x.slot[bank][rank][0], q), rb = mapa(&x.bar[bank], q);
+        st_async2(ra, At, Bt[0], rb);
+        if (NV == 2) st_async1(ra + 16, Bt[NV - 1], rb);
+    }
+    // one warp spins on the mbarrier, the others sleep in the block barrier
+    if (threadIdx.x < 32 && (FWD ? rank > 0 : rank < C - 1)) mbar_wait(&x.bar[bank], 0);
+    __syncthreads();
+#pragma unroll
+    for (int v = 0; v < NV; ++v) carry[v] = 0.0;
+    if (FWD) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+            if (r < rank) {
+                const double a = x.slot[0][r][0];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) carry[v] = a * carry[v] + x.slot[0][r][1 + v];
+            }
+    } else {
+#pragma unroll
+        for (int r = 7; r >= 0; --r)
+            if (r > rank && r < C) {
+                const double a = x.slot[1][r][0];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) carry[v] = a * carry[v] + x.slot[1][r][1 + v];
+            }
+    }
+}
+
+
+// Pull variant (radial lines, measured faster there): each CTA publishes its
+// total locally, one cluster barrier, remote loads of the earlier (later)
+// ranks' slots; the backward pass ends with a barrier so no CTA exits while
+// its slot is read.
+template <int NV, bool FWD>
+__device__ __forceinline__ void cluster_carry_pull(double At, const double (&Bt)[NV], ClX& x,
+                                                   double (&carry)[NV]) {
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = cl.block_rank(), C = cl.num_blocks();
+    double* slot = &x.slot[FWD ? 0 : 1][0][0];
     if (threadIdx.x == 0) {
         slot[0] = At;
 #pragma unroll
         for (int v = 0; v < NV; ++v) slot[1 + v] = Bt[v];
     }
     cl.sync();
-    // all remote slots loaded first (independent DSMEM loads in flight), then
-    // composed in rank order
     double ra[8], rb[8][NV];
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
@@ -1886,10 +1975,10 @@ __device__ __forceinline__ void cluster_carry(double At, const double (&Bt)[NV],
 #pragma unroll
         for (int v = 0; v < NV; ++v) rb[r][v] = 0.0;
         if (use) {
-            const double* x = cl.map_shared_rank(slot, r);
-            ra[r] = x[0];
+            const double* q = cl.map_shared_rank(slot, r);
+            ra[r] = q[0];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) rb[r][v] = x[1 + v];
+            for (int v = 0; v < NV; ++v) rb[r][v] = q[1 + v];
         }
     }
 #pragma unroll
@@ -1904,17 +1993,20 @@ __device__ __forceinline__ void cluster_carry(double At, const double (&Bt)[NV],
         for (int r = 7; r >= 0; --r)
 #pragma unroll
             for (int v = 0; v < NV; ++v) carry[v] = ra[r] * carry[v] + rb[r][v];
+        cl.sync();
     }
-    if (!FWD) cl.sync();  // remote reads done before any CTA of the cluster exits
 }
 
-// Solve of rows [row0, row0+nloc) of an ntot-row LL^T (+ SM) line held by a
-// cluster.  Y: local rhs in / x out; IL: 1/l; Mx[P(j)] = m_{row0+j-1}
-// (j = 0..nloc; 0 before global row 0).  xch: 8 doubles of exchange space.
+// seg: rows per independent line when the cluster holds two lines back to
+// back (ntot = 2 seg; the recurrences restart at row seg), else ntot.
+// Circle (CYC) lines exchange chunk totals by st.async pushes, radial lines
+// by the pull variant (each measured faster on its own lines).
 template <int K, bool CYC>
 __device__ __forceinline__ void line_solve_cl(double* Y, const double* IL, const double* Mx,
                                               int nloc, int row0, int ntot, double corner,
-                                              double* scr, double* xch) {
+                                              double* scr, ClX& xch, int seg) {
+    auto first = [&](int g) { return g == 0 || g == seg; };
+    auto last = [&](int g) { return g == seg - 1 || g == ntot - 1; };
     constexpr int NV = CYC ? 2 : 1;
     const int j0 = threadIdx.x * K;
     double y[K], z[CYC ? K : 1];
@@ -1926,7 +2018,7 @@ __device__ __forceinline__ void line_solve_cl(double* Y, const double* IL, const
         const int j = j0 + q, g = row0 + j;
         if (j < nloc) {
             const double il = IL[P(j)];
-            const double a = g > 0 ? -(Mx[P(j)] * il) : 0.0;
+            const double a = !first(g) ? -(Mx[P(j)] * il) : 0.0;
             const double b = Y[P(j)];
             y[q] = b;
             Bv[0] = a * Bv[0] + b * il;
@@ -1936,7 +2028,7 @@ __device__ __forceinline__ void line_solve_cl(double* Y, const double* IL, const
     }
     double Aex, Bex[NV], At, Bt[NV], carry[NV];
     block_scan_ex<NV, true>(A, Bv, Aex, Bex, At, Bt, scr);
-    cluster_carry<NV, true>(At, Bt, xch, carry);
+    if (CYC) cluster_carry<NV, true>(At, Bt, xch, carry); else cluster_carry_pull<NV, true>(At, Bt, xch, carry);
     {
         double yp = Aex * carry[0] + Bex[0], zp = Aex * carry[NV - 1] + Bex[NV - 1];
 #pragma unroll
@@ -1944,7 +2036,7 @@ __device__ __forceinline__ void line_solve_cl(double* Y, const double* IL, const
             const int j = j0 + q, g = row0 + j;
             if (j < nloc) {
                 const double il = IL[P(j)];
-                const double mp = g > 0 ? Mx[P(j)] : 0.0;
+                const double mp = !first(g) ? Mx[P(j)] : 0.0;
                 yp = (y[q] - mp * yp) * il;
                 y[q] = yp;
                 if (CYC) {
@@ -1962,14 +2054,14 @@ __device__ __forceinline__ void line_solve_cl(double* Y, const double* IL, const
         const int j = j0 + q, g = row0 + j;
         if (j < nloc) {
             const double il = IL[P(j)];
-            const double gg = g < ntot - 1 ? -(Mx[P(j + 1)] * il) : 0.0;
+            const double gg = !last(g) ? -(Mx[P(j + 1)] * il) : 0.0;
             Dv[0] = gg * Dv[0] + y[q] * il;
             if (CYC) Dv[NV - 1] = gg * Dv[NV - 1] + z[CYC ? q : 0] * il;
             G = gg * G;
         }
     }
     block_scan_ex<NV, false>(G, Dv, Aex, Bex, At, Bt, scr);
-    cluster_carry<NV, false>(At, Bt, xch, carry);
+    if (CYC) cluster_carry<NV, false>(At, Bt, xch, carry); else cluster_carry_pull<NV, false>(At, Bt, xch, carry);
     {
         double xp = Aex * carry[0] + Bex[0], zq = Aex * carry[NV - 1] + Bex[NV - 1];
 #pragma unroll
@@ -1977,7 +2069,7 @@ __device__ __forceinline__ void line_solve_cl(double* Y, const double* IL, const
             const int j = j0 + q, g = row0 + j;
             if (j < nloc) {
                 const double il = IL[P(j)];
-                const double mj = g < ntot - 1 ? Mx[P(j + 1)] : 0.0;
+                const double mj = !last(g) ? Mx[P(j + 1)] : 0.0;
                 xp = (y[q] - mj * xp) * il;
                 y[q] = xp;
                 if (CYC) {
@@ -1988,27 +2080,26 @@ __device__ __forceinline__ void line_solve_cl(double* Y, const double* IL, const
         }
     }
     if (CYC) {
-        // x, z at global rows 0 (rank 0) and ntot-1 (last rank), via DSMEM
+        // x, z at global rows 0 (rank 0) and ntot-1 (last rank), pushed into
+        // every CTA of the cluster
         cg::cluster_group cl = cg::this_cluster();
-        const int rank = cl.block_rank(), C = cl.num_blocks();
+        const int C = cl.num_blocks(), rank = cl.block_rank();
+        double* ends = xch.ends;
 #pragma unroll
         for (int q = 0; q < K; ++q) {
             const int j = j0 + q, g = row0 + j;
-            if (j < nloc && g == 0) {
-                xch[4] = y[q];
-                xch[5] = z[CYC ? q : 0];
-            }
-            if (j < nloc && g == ntot - 1) {
-                xch[6] = y[q];
-                xch[7] = z[CYC ? q : 0];
+            if (j < nloc && (g == 0 || g == ntot - 1)) {
+                const int e = g == 0 ? 0 : 2;
+                ends[e] = y[q];
+                ends[e + 1] = z[CYC ? q : 0];
+                for (int r = 0; r < C; ++r)
+                    if (r != rank)
+                        st_async2(mapa(&ends[e], r), y[q], z[CYC ? q : 0], mapa(&xch.bar[2], r));
             }
         }
-        cl.sync();
-        const double* x0 = cl.map_shared_rank(xch, 0);
-        const double* xl = cl.map_shared_rank(xch, C - 1);
-        const double tau = corner * (x0[4] + xl[6]) / (1.0 + corner * (x0[5] + xl[7]));
-        (void)rank;
-        cl.sync();
+        if (threadIdx.x < 32) mbar_wait(&xch.bar[2], 0);  // C > 1: at least one end row arrives
+        __syncthreads();  // (and this CTA's own end rows are written)
+        const double tau = corner * (ends[0] + ends[2]) / (1.0 + corner * (ends[1] + ends[3]));
 #pragma unroll
         for (int q = 0; q < K; ++q) y[q] -= tau * z[CYC ? q : 0];
     }
@@ -2033,7 +2124,7 @@ __global__ void __launch_bounds__(256, PMG_CL_MINB) k_radial_cl(LevelView L, dou
                                                    const int* __restrict__ active) {
     pdl_enter();
     extern __shared__ double smem[];
-    __shared__ double xch[8];
+    __shared__ ClX xch;
     cg::cluster_group cl = cg::this_cluster();
     const int C = cl.num_blocks(), rank = cl.block_rank();
     const int b = blockIdx.y;
@@ -2069,6 +2160,10 @@ __global__ void __launch_bounds__(256, PMG_CL_MINB) k_radial_cl(LevelView L, dou
     const double* __restrict__ ART = L.art + off;
     const int N = L.nr - 1;
     const CoefAt<false> cf{&L, off, b};
+#ifdef PMG_DIAG_NOGATHER
+    for (int j = threadIdx.x; j < nloc; j += T) Y[P(j)] = F[base + row0 + j];
+    if (false)
+#endif
 #pragma unroll 2
     for (int j = threadIdx.x; j < nloc; j += T) {
         const int i = row0 + j, s = split + i, p = base + i;
@@ -2116,7 +2211,9 @@ __global__ void __launch_bounds__(256, PMG_CL_MINB) k_radial_cl(LevelView L, dou
     __pipeline_wait_prior(0);
     for (int j = threadIdx.x; j < nloc; j += T) IL[P(j)] = __drcp_rn(IL[P(j)]);
     __syncthreads();
-    line_solve_cl<K, false>(Y, IL, Mx, nloc, row0, len, 0.0, scr, xch);
+#ifndef PMG_DIAG_NOSOLVE
+    line_solve_cl<K, false>(Y, IL, Mx, nloc, row0, len, 0.0, scr, xch, len);
+#endif
     for (int j = threadIdx.x; j < nloc; j += T) U[base + row0 + j] = Y[P(j)];
 }
 
@@ -2131,7 +2228,7 @@ __global__ void __launch_bounds__(256, PMG_CL_MINB) k_circle_cl(LevelView L, dou
                                                    const int* __restrict__ active) {
     pdl_enter();
     extern __shared__ double smem[];
-    __shared__ double xch[8];
+    __shared__ ClX xch;
     cg::cluster_group cl = cg::this_cluster();
     const int C = cl.num_blocks(), rank = cl.block_rank();
     const int b = blockIdx.y;
@@ -2154,6 +2251,7 @@ __global__ void __launch_bounds__(256, PMG_CL_MINB) k_circle_cl(LevelView L, dou
     double* Mx = IL + pn;
     double* scr = Mx + pn;
     const long fo = (long)b * L.split * nt + (long)s * nt;
+    clx_init<2, true>(xch);
     // line factors: asynchronous copies overlapped with the rhs gather
     for (int j = threadIdx.x; j < nloc; j += T)
         __pipeline_memcpy_async(&IL[P(j)], &cil[fo + row0 + j], 8);
@@ -2190,7 +2288,8 @@ __global__ void __launch_bounds__(256, PMG_CL_MINB) k_circle_cl(LevelView L, dou
     __pipeline_wait_prior(0);
     for (int j = threadIdx.x; j < nloc; j += T) IL[P(j)] = __drcp_rn(IL[P(j)]);
     __syncthreads();
-    line_solve_cl<K, true>(Y, IL, Mx, nloc, row0, nt, corner[(long)b * L.split + s], scr, xch);
+    clx_ready();
+    line_solve_cl<K, true>(Y, IL, Mx, nloc, row0, nt, corner[(long)b * L.split + s], scr, xch, nt);
     for (int j = threadIdx.x; j < nloc; j += T) U[base + row0 + j] = Y[P(j)];
 }
 
