@@ -109,6 +109,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
         : "memory");
 }
 
+// loads of u inside a launch whose other CTAs write u (fused smoothing) go
+// through L2 (ld.global.cg): L1 is not coherent across SMs
+template <bool CG>
+__device__ __forceinline__ double ldu(const double* p) {
+    if (CG) return __ldcg(p);
+    return *p;
+}
 __device__ __forceinline__ int P(int i) { return i + (i >> 4); }  // bank-conflict padding
 __host__ __device__ __forceinline__ int padded(int n) { return n + (n >> 4) + 1; }
 
@@ -718,6 +725,7 @@ __device__ __forceinline__ bool circle_lean_ring(const LevelView& L, int s) {
 #endif
     return s >= 1 && s + 1 < L.split && s + 1 < L.nr - 1 && !(s == 1 && L.boundary == 1);
 }
+template <bool CG = false>
 __device__ __forceinline__ double circle_rhs_lean(const LevelView& L, long off, int s, int t,
                                                   const double* __restrict__ U,
                                                   const double* __restrict__ F) {
@@ -728,9 +736,9 @@ __device__ __forceinline__ double circle_rhs_lean(const LevelView& L, long off, 
     const double* R = L.art + off;
     const double aP = A[p], aSM = A[p - nt], aSP = A[p + nt];
     const double rTM = R[pTM], rTP = R[pTP], rSM = R[p - nt], rSP = R[p + nt];
-    const double uSM = U[p - nt], uSP = U[p + nt];
-    const double uSMTM = U[pTM - nt], uSMTP = U[pTP - nt];
-    const double uSPTM = U[pTM + nt], uSPTP = U[pTP + nt];
+    const double uSM = ldu<CG>(&U[p - nt]), uSP = ldu<CG>(&U[p + nt]);
+    const double uSMTM = ldu<CG>(&U[pTM - nt]), uSMTP = ldu<CG>(&U[pTP - nt]);
+    const double uSPTM = ldu<CG>(&U[pTM + nt]), uSPTP = ldu<CG>(&U[pTP + nt]);
     const double fP = F[p];
     const double kbar = 0.5 * (L.k[tm] + L.k[t]);
     const double qkm = xdiv(kbar, L.h[s - 1], L.rh[s - 1]);
@@ -1537,22 +1545,18 @@ __global__ void __launch_bounds__(288, PMG_TMA_MINB) k_apply_tma(LevelView L, Tm
 // rhs_t = f - sum_{off-line} A u (smoother.cpp:162-182), then the cyclic
 // Sherman-Morrison solve (line_algebra.cpp:98-120), or the envelope solve of
 // the across-origin ring 0 (smoother.cpp:144-152).
-template <bool ONFLY, int K>
-__global__ void __launch_bounds__(512) k_circle(LevelView L, double* __restrict__ u,
-                                                const double* __restrict__ f,
-                                                const double* __restrict__ cil,
-                                                const double* __restrict__ cm,
-                                                const double* __restrict__ corner,
-                                                const double* __restrict__ cz,
-                                                OriginFactor of, int parity, int serial,
-                                                int exact_rings,
-                                                const int* __restrict__ active) {
-    KT(0);
-    pdl_enter();
-    extern __shared__ double smem[];
-    const int b = blockIdx.y;
-    if (active && !active[b]) return;
-    const int s = parity + 2 * blockIdx.x;
+// One circle line (ring s of section b), reference smoother.cpp:95-116,
+// 144-182: rhs gather, then the cyclic Sherman-Morrison solve
+// (line_algebra.cpp:98-120) or the envelope solve of the across-origin ring.
+template <bool ONFLY, int K, bool CG>
+__device__ __forceinline__ void circle_body(const LevelView& L, double* __restrict__ u,
+                                            const double* __restrict__ f,
+                                            const double* __restrict__ cil,
+                                            const double* __restrict__ cm,
+                                            const double* __restrict__ corner,
+                                            const double* __restrict__ cz,
+                                            const OriginFactor& of, int serial, int exact_rings,
+                                            int b, int s, double* smem) {
     const int nt = L.nt, T = blockDim.x;
     const long off = (long)b * L.n;
     double* U = u + off;
@@ -1586,31 +1590,31 @@ __global__ void __launch_bounds__(512) k_circle(LevelView L, double* __restrict_
             const int p = base + t;
             const Nbr q = neighbours(L, s, t, p);
             double acc = F[p];
-            acc -= Rw[1 * n + p] * U[q.pSM];
-            acc -= Rw[2 * n + p] * U[q.pSP];
-            acc -= Rw[5 * n + p] * U[q.pSMTM];
-            acc -= Rw[6 * n + p] * U[q.pSMTP];
-            acc -= Rw[7 * n + p] * U[q.pSPTM];
-            acc -= Rw[8 * n + p] * U[q.pSPTP];
+            acc -= Rw[1 * n + p] * ldu<CG>(&U[q.pSM]);
+            acc -= Rw[2 * n + p] * ldu<CG>(&U[q.pSP]);
+            acc -= Rw[5 * n + p] * ldu<CG>(&U[q.pSMTM]);
+            acc -= Rw[6 * n + p] * ldu<CG>(&U[q.pSMTP]);
+            acc -= Rw[7 * n + p] * ldu<CG>(&U[q.pSPTM]);
+            acc -= Rw[8 * n + p] * ldu<CG>(&U[q.pSPTP]);
             Y[P(t)] = acc;
         }
     } else if (!ONFLY && circle_lean_ring(L, s)) {
-        for (int t = threadIdx.x; t < nt; t += T) Y[P(t)] = circle_rhs_lean(L, off, s, t, U, F);
+        for (int t = threadIdx.x; t < nt; t += T) Y[P(t)] = circle_rhs_lean<CG>(L, off, s, t, U, F);
     } else
     for (int t = threadIdx.x; t < nt; t += T) {
         const int p = base + t;
         const Nbr q = neighbours(L, s, t, p);
         const Row R = make_row_fast(L, cf, s, t, p, q);
         double acc = F[p];
-        if (R.has_sm) acc -= R.sm * U[q.pSM];
-        if (R.has_sp) acc -= R.sp * U[q.pSP];
+        if (R.has_sm) acc -= R.sm * ldu<CG>(&U[q.pSM]);
+        if (R.has_sp) acc -= R.sp * ldu<CG>(&U[q.pSP]);
         if (R.has_sm) {
-            acc -= R.mm * U[q.pSMTM];
-            acc -= R.mp * U[q.pSMTP];
+            acc -= R.mm * ldu<CG>(&U[q.pSMTM]);
+            acc -= R.mp * ldu<CG>(&U[q.pSMTP]);
         }
         if (R.has_sp) {
-            acc -= R.pm * U[q.pSPTM];
-            acc -= R.pp * U[q.pSPTP];
+            acc -= R.pm * ldu<CG>(&U[q.pSPTM]);
+            acc -= R.pp * ldu<CG>(&U[q.pSPTP]);
         }
         Y[P(t)] = acc;
     }
@@ -1634,7 +1638,24 @@ __global__ void __launch_bounds__(512) k_circle(LevelView L, double* __restrict_
     }
     KT(4);
     for (int t = threadIdx.x; t < nt; t += T) U[base + t] = Y[P(t)];
-    KT(5);
+    KT(5);}
+template <bool ONFLY, int K>
+__global__ void __launch_bounds__(512) k_circle(LevelView L, double* __restrict__ u,
+                                                const double* __restrict__ f,
+                                                const double* __restrict__ cil,
+                                                const double* __restrict__ cm,
+                                                const double* __restrict__ corner,
+                                                const double* __restrict__ cz,
+                                                OriginFactor of, int parity, int serial,
+                                                int exact_rings,
+                                                const int* __restrict__ active) {
+    KT(0);
+    pdl_enter();
+    extern __shared__ double smem[];
+    const int b = blockIdx.y;
+    if (active && !active[b]) return;
+    circle_body<ONFLY, K, false>(L, u, f, cil, cm, corner, cz, of, serial, exact_rings, b,
+                                 parity + 2 * blockIdx.x, smem);
 }
 
 // ------------------------------------------------------------- radial sweep
@@ -1642,18 +1663,14 @@ __global__ void __launch_bounds__(512) k_circle(LevelView L, double* __restrict_
 // rhs over rings split..n_r-1 (smoother.cpp:184-205) then the tridiagonal
 // Cholesky solve (line_algebra.cpp:42-62); the Dirichlet row rides along as
 // an identity row.
-template <bool ONFLY, int K>
-__global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict__ u,
-                                                const double* __restrict__ f,
-                                                const double* __restrict__ ril,
-                                                const double* __restrict__ rm, int parity,
-                                                int serial, const int* __restrict__ active) {
-    KT(0);
-    pdl_enter();
-    extern __shared__ double smem[];
-    const int b = blockIdx.y;
-    if (active && !active[b]) return;
-    const int t = parity + 2 * blockIdx.x;
+// One radial line (spoke t of section b), reference smoother.cpp:118-142,
+// 184-205: rhs gather, then the tridiagonal LL^T solve (line_algebra.cpp:42-62).
+template <bool ONFLY, int K, bool CG>
+__device__ __forceinline__ void radial_body(const LevelView& L, double* __restrict__ u,
+                                            const double* __restrict__ f,
+                                            const double* __restrict__ ril,
+                                            const double* __restrict__ rm, int serial, int b,
+                                            int t, double* smem) {
     const int len = L.len, split = L.split, T = blockDim.x;
     const long off = (long)b * L.n;
     double* U = u + off;
@@ -1684,13 +1701,13 @@ __global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict_
             const int s = split + i, p = base + i;
             const Nbr q = neighbours(L, s, t, p);
             double acc = F[p];
-            if (s == split) acc -= Rw[1 * n + p] * U[q.pSM];
-            acc -= Rw[3 * n + p] * U[q.pTM];
-            acc -= Rw[4 * n + p] * U[q.pTP];
-            acc -= Rw[5 * n + p] * U[q.pSMTM];
-            acc -= Rw[6 * n + p] * U[q.pSMTP];
-            acc -= Rw[7 * n + p] * U[q.pSPTM];
-            acc -= Rw[8 * n + p] * U[q.pSPTP];
+            if (s == split) acc -= Rw[1 * n + p] * ldu<CG>(&U[q.pSM]);
+            acc -= Rw[3 * n + p] * ldu<CG>(&U[q.pTM]);
+            acc -= Rw[4 * n + p] * ldu<CG>(&U[q.pTP]);
+            acc -= Rw[5 * n + p] * ldu<CG>(&U[q.pSMTM]);
+            acc -= Rw[6 * n + p] * ldu<CG>(&U[q.pSMTP]);
+            acc -= Rw[7 * n + p] * ldu<CG>(&U[q.pSPTM]);
+            acc -= Rw[8 * n + p] * ldu<CG>(&U[q.pSPTP]);
             Y[P(i)] = acc;
         }
         ifirst = len;
@@ -1709,9 +1726,9 @@ __global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict_
             const double attP = ATT[p], attM = ATT[p + dTM], attQ = ATT[p + dTP];
             const double artM = ART[p + dTM], artQ = ART[p + dTP];
             const double artSM = ART[p - 1], artSP = ART[p + 1];
-            const double uM = U[p + dTM], uQ = U[p + dTP];
-            const double uMM = U[p + dTM - 1], uQM = U[p + dTP - 1];
-            const double uMP = U[p + dTM + 1], uQP = U[p + dTP + 1];
+            const double uM = ldu<CG>(&U[p + dTM]), uQ = ldu<CG>(&U[p + dTP]);
+            const double uMM = ldu<CG>(&U[p + dTM - 1]), uQM = ldu<CG>(&U[p + dTP - 1]);
+            const double uMP = ldu<CG>(&U[p + dTM + 1]), uQP = ldu<CG>(&U[p + dTP + 1]);
             const double hbar = 0.5 * (L.h[s - 1] + L.h[s]);
             const double south = -xdiv(hbar, km, rkm) * (attP + attM);
             const double north = -xdiv(hbar, kp, rkp) * (attP + attQ);
@@ -1741,16 +1758,16 @@ __global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict_
         const Nbr q = neighbours(L, s, t, p);
         const Row R = make_row_fast(L, cf, s, t, p, q);
         double acc = F[p];
-        if (s == split && R.has_sm) acc -= R.sm * U[q.pSM];
-        acc -= R.tm * U[q.pTM];
-        acc -= R.tp * U[q.pTP];
+        if (s == split && R.has_sm) acc -= R.sm * ldu<CG>(&U[q.pSM]);
+        acc -= R.tm * ldu<CG>(&U[q.pTM]);
+        acc -= R.tp * ldu<CG>(&U[q.pTP]);
         if (R.has_sm) {
-            acc -= R.mm * U[q.pSMTM];
-            acc -= R.mp * U[q.pSMTP];
+            acc -= R.mm * ldu<CG>(&U[q.pSMTM]);
+            acc -= R.mp * ldu<CG>(&U[q.pSMTP]);
         }
         if (R.has_sp) {
-            acc -= R.pm * U[q.pSPTM];
-            acc -= R.pp * U[q.pSPTP];
+            acc -= R.pm * ldu<CG>(&U[q.pSPTM]);
+            acc -= R.pp * ldu<CG>(&U[q.pSPTP]);
         }
         Y[P(i)] = acc;
     }
@@ -1768,7 +1785,19 @@ __global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict_
     }
     KT(4);
     for (int i = threadIdx.x; i < len; i += T) U[base + i] = Y[P(i)];
-    KT(5);
+    KT(5);}
+template <bool ONFLY, int K>
+__global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict__ u,
+                                                const double* __restrict__ f,
+                                                const double* __restrict__ ril,
+                                                const double* __restrict__ rm, int parity,
+                                                int serial, const int* __restrict__ active) {
+    KT(0);
+    pdl_enter();
+    extern __shared__ double smem[];
+    const int b = blockIdx.y;
+    if (active && !active[b]) return;
+    radial_body<ONFLY, K, false>(L, u, f, ril, rm, serial, b, parity + 2 * blockIdx.x, smem);
 }
 
 // ------------------------------------------------- cluster-split line solves
@@ -2291,6 +2320,92 @@ __global__ void __launch_bounds__(256, PMG_CL_MINB) k_circle_cl(LevelView L, dou
     clx_ready();
     line_solve_cl<K, true>(Y, IL, Mx, nloc, row0, nt, corner[(long)b * L.split + s], scr, xch, nt);
     for (int j = threadIdx.x; j < nloc; j += T) U[base + row0 + j] = Y[P(j)];
+}
+
+
+// ------------------------------------------------------ fused smoothing step
+// Dependencies (reference smoother.cpp:72-81 order, Gauss-Seidel in place):
+// a white ring needs the black rings s-1, s+1; a black spoke needs ring
+// split-1 (its row split couples to it, and ring split-1 reads row split
+// before the spokes overwrite it); a white spoke needs the black spokes
+// t-1, t+1.  Black rings need nothing: the white lines they read are not
+// written before they are done, since those wait for them.
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <bool ONFLY, int K>
+__global__ void __launch_bounds__(512) k_smooth_fused(LevelView L, double* __restrict__ u,
+                                                      const double* __restrict__ f,
+                                                      const double* __restrict__ cil,
+                                                      const double* __restrict__ cm,
+                                                      const double* __restrict__ corner,
+                                                      const double* __restrict__ cz,
+                                                      OriginFactor of,
+                                                      const double* __restrict__ ril,
+                                                      const double* __restrict__ rm,
+                                                      int exact_rings, FuseCtl fc,
+                                                      const int* __restrict__ order, int nitems,
+                                                      const int* __restrict__ active) {
+    pdl_enter();
+    extern __shared__ double smem[];
+    __shared__ int s_item;
+    __shared__ unsigned s_epoch;
+    if (threadIdx.x == 0) {
+        s_item = order[atomicAdd(&fc.ctl[0], 1u)];
+        s_epoch = *reinterpret_cast<volatile unsigned*>(&fc.ctl[2]);
+    }
+    __syncthreads();
+    const int per = L.split + L.nt;
+    const int item = s_item, b = item / per, c = item - b * per;
+    const unsigned ep = s_epoch;
+    unsigned* flags = fc.flags + (long)b * per;
+    if (!active || active[b]) {
+        if (threadIdx.x == 0) {
+            int dep[2] = {-1, -1};
+            if (c < L.split) {
+                if (c & 1) {  // white ring
+                    dep[0] = c - 1;
+                    dep[1] = c + 1 < L.split ? c + 1 : -1;
+                }
+            } else {
+                const int t = c - L.split;
+                if (t & 1) {  // white spoke
+                    dep[0] = L.split + t - 1;
+                    dep[1] = L.split + (t + 1 == L.nt ? 0 : t + 1);
+                } else {
+                    dep[0] = L.split - 1;
+                }
+            }
+            for (int d = 0; d < 2; ++d)
+                if (dep[d] >= 0)
+                    while (ld_acquire(&flags[dep[d]]) != ep) __nanosleep(32);
+        }
+        __syncthreads();
+        if (c < L.split)
+            circle_body<ONFLY, K, true>(L, u, f, cil, cm, corner, cz, of, 0, exact_rings, b, c, smem);
+        else
+            radial_body<ONFLY, K, true>(L, u, f, ril, rm, 0, b, c - L.split, smem);
+        __syncthreads();  // every thread's stores of the line issued
+        if (threadIdx.x == 0) {
+            __threadfence();
+            st_release(&flags[c], ep);
+        }
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&fc.ctl[1], 1u) == (unsigned)nitems - 1) {  // last CTA: reset for the next launch
+            fc.ctl[0] = 0;
+            fc.ctl[1] = 0;
+            __threadfence();
+            atomicAdd(&fc.ctl[2], 1u);
+        }
+    }
 }
 
 // ---------------------------------------------------------------- transfers
@@ -3512,6 +3627,65 @@ void launch_radial(const LevelView& L, bool onfly, double* u, const double* f, c
         default: PMG_R(16); break;
     }
 #undef PMG_R
+}
+
+bool fused_ok(const LevelView& L, bool serial, int exact_rings) {
+    static const bool on = [] {
+        const char* e = std::getenv("PMG_FUSED_SMOOTH");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    return on && !serial && exact_rings <= 0 && L.len > 1 && L.split >= 2 && L.nt <= 1024 &&
+           L.len <= 1024 && (L.nt & 1) == 0;
+}
+
+void fused_order(int split, int nt, int B, int* out) {
+    // black rings from the outside in (ring split-1, which the spokes wait
+    // for, first), white rings, black spokes, white spokes; sections
+    // interleaved within each phase
+    const int per = split + nt;
+    long k = 0;
+    for (int s = (split - 1) & ~1; s >= 0; s -= 2)
+        for (int b = 0; b < B; ++b) out[k++] = b * per + s;
+    for (int s = (split - 1) | 1; s >= 1; s -= 2) {
+        if (s >= split) continue;
+        for (int b = 0; b < B; ++b) out[k++] = b * per + s;
+    }
+    for (int t = 0; t < nt; t += 2)
+        for (int b = 0; b < B; ++b) out[k++] = b * per + split + t;
+    for (int t = 1; t < nt; t += 2)
+        for (int b = 0; b < B; ++b) out[k++] = b * per + split + t;
+}
+
+void launch_smooth_fused(const LevelView& L, bool onfly, double* u, const double* f,
+                         const double* cil, const double* cm, const double* corner,
+                         const double* cz, const OriginFactor& of, const double* ril,
+                         const double* rm, int exact_rings, const FuseCtl& fc, const int* order,
+                         const int* active, cudaStream_t st) {
+    const int n = std::max(L.nt, L.len);
+    const int nitems = (L.split + L.nt) * L.B;
+    int K, T;
+    line_shape(n, K, T, nitems);
+    const size_t sm = line_smem(n);
+#define PMG_F(ON, KK)                                                                          \
+    do {                                                                                       \
+        set_smem(k_smooth_fused<ON, KK>, sm);                                                  \
+        launch_k(k_smooth_fused<ON, KK>, dim3(nitems), T, sm, st, L, u, f, cil, cm, corner, cz, \
+                 of, ril, rm, exact_rings, fc, order, nitems, active);                         \
+    } while (0)
+#define PMG_FK(ON)                       \
+    switch (K) {                         \
+        case 2: PMG_F(ON, 2); break;     \
+        case 4: PMG_F(ON, 4); break;     \
+        case 8: PMG_F(ON, 8); break;     \
+        default: PMG_F(ON, 16); break;   \
+    }
+    if (onfly) {
+        PMG_FK(true)
+    } else {
+        PMG_FK(false)
+    }
+#undef PMG_FK
+#undef PMG_F
 }
 
 void launch_restrict(const LevelView& F, const LevelView& C, const Weights& w, const double* fr,

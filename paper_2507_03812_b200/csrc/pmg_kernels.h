@@ -162,6 +162,25 @@ void launch_radial(const LevelView& L, bool onfly, double* u, const double* f, c
                    const double* rm, int parity, bool serial, const int* active,
                    cudaStream_t st);
 
+// Fused smoothing step (all four zebra sweeps of one level in ONE launch) for
+// levels whose lines run one CTA each.  Lines are claimed through a ticket
+// counter in a host-built order (fused_order) in which every line comes after
+// the lines it must wait for; a CTA waits on the epoch-stamped completion
+// flags of those lines, solves its line and stamps its own flag.
+struct FuseCtl {
+    unsigned* ctl;     // [0] ticket, [1] done, [2] epoch (starts at 1)
+    unsigned* flags;   // [B][split + nt] completion epochs of rings, then spokes
+};
+bool fused_ok(const LevelView& L, bool serial, int exact_rings);
+// claim order of the B*(split+nt) lines (codes b*(split+nt) + c; c < split:
+// ring c, else spoke c - split)
+void fused_order(int split, int nt, int B, int* out);
+void launch_smooth_fused(const LevelView& L, bool onfly, double* u, const double* f,
+                         const double* cil, const double* cm, const double* corner,
+                         const double* cz, const OriginFactor& of, const double* ril,
+                         const double* rm, int exact_rings, const FuseCtl& fc, const int* order,
+                         const int* active, cudaStream_t st);
+
 // mask: zero the coarse Dirichlet rows (mask_dirichlet_rows, multigrid.cpp:146-153)
 void launch_restrict(const LevelView& F, const LevelView& C, const Weights& w, const double* fr,
                      double* cf, double* cu_zero, bool mask, const int* active, cudaStream_t st);

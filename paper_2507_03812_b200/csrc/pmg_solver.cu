@@ -184,6 +184,9 @@ struct Level {
     Weights w{};
     EnvFactor env{};
     OriginFactor of() const { return OriginFactor{ob1, ob2, or1, or2, oD, ofc1, ofc2}; }
+    // fused smoothing step (fused_ok levels): claim order and completion flags
+    int* forder = nullptr;
+    unsigned* fflags = nullptr;
 };
 
 struct Solver {
@@ -351,6 +354,7 @@ struct Solver {
         setup_rows();
         setup_coarse_tail();
         setup_mid();
+        setup_fused();
         if (set.extrapolation) ex_g = alloc<double>((size_t)B * lv[0].v.n);
         // convergence state
         hist_cap = std::max(set.max_iterations, 0) + 1;
@@ -717,12 +721,42 @@ struct Solver {
         }
     }
 
+    // Fused smoothing steps: levels with one-CTA lines run all four zebra
+    // sweeps in one launch (launch_smooth_fused); one control block (ticket,
+    // done count, epoch) serves every launch since they are stream-ordered.
+    unsigned* fuse_ctl = nullptr;
+    void setup_fused() {
+        for (size_t l = 0; l < lv.size(); ++l) {
+            Level& V = lv[l];
+            if (coarse_start >= 0 && (int)l >= coarse_start) break;  // resident tail
+            if (l == 0 && set.extrapolation) continue;
+            if (!fused_ok(V.v, serial, exact_rings)) continue;
+            // large batches keep the per-colour launches (c3, 256 sections:
+            // 14% slower fused -- ticket contention over 152K lines)
+            if ((long)B * (V.v.split + V.v.nt) > 16384) continue;
+            if (!fuse_ctl) {
+                fuse_ctl = alloc<unsigned>(4);
+                const unsigned init[4] = {0u, 0u, 1u, 0u};
+                PMG_CUDA(cudaMemcpyAsync(fuse_ctl, init, sizeof init, cudaMemcpyHostToDevice,
+                                         stream));
+            }
+            const int per = V.v.split + V.v.nt;
+            std::vector<int> order((size_t)B * per);
+            fused_order(V.v.split, V.v.nt, B, order.data());
+            V.forder = upload(order);
+            V.fflags = alloc<unsigned>((size_t)B * per);
+        }
+        PMG_CUDA(cudaStreamSynchronize(stream));
+    }
+
     // Cluster-wide sub-cycle (k_mid_cycle): the levels just above the resident
     // tail whose lines fit a warp and whose vectors stay in L2 run in one
-    // launch per cycle, one thread-block cluster per section.
+    // launch per cycle, one thread-block cluster per section.  Opt-in
+    // (PMG_MID_NODES=5000): measured 1-2% slower than the per-level kernels on
+    // c0, c1, c2-V and c2-W once those got faster.
     void setup_mid() {
         if (coarse_start <= 0 || serial) return;
-        long max_nodes = 5000;
+        long max_nodes = 0;
         if (const char* e = std::getenv("PMG_MID_NODES")) max_nodes = std::atol(e);
         int max_b = 16;
         if (const char* e = std::getenv("PMG_MID_SECTIONS")) max_b = std::atoi(e);
@@ -1009,6 +1043,14 @@ struct Solver {
                     launch_radial(V.v, onfly, V.u, ex_g, V.ril, V.rm, 1, serial, act, stream);
                 });
             run(KK_SMOOTH, 3, [&] { launch_ex_pointwise(V.v, onfly, V.u, V.f, act, stream); });
+            return;
+        }
+        if (V.forder) {
+            run(KK_SMOOTH, 1, [&] {
+                launch_smooth_fused(V.v, onfly, V.u, V.f, V.cil, V.cm, V.corner, V.cz, V.of(),
+                                    V.ril, V.rm, exact_rings, FuseCtl{fuse_ctl, V.fflags},
+                                    V.forder, act, stream);
+            });
             return;
         }
         for (int parity = 0; parity < 2; ++parity)

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round evidence on one B200: bench lines, reference arm, ncu launch lists and
 # --set full captures of the finest-level kernels.  usage: bash tools/profile_round.sh <out>
-out=${1:-gpurun_out/r01}
+out=${1:-gpurun_out/r01b}
 mkdir -p $out
 nvidia-smi --query-gpu=name,driver_version,clocks.max.sm,memory.total --format=csv > $out/gpu.txt
 lscpu | grep -E "Model name|^CPU\(s\)|Thread|Core" > $out/host.txt
