@@ -1179,7 +1179,7 @@ __device__ __forceinline__ bool lean_ring(const LevelView& L, int s) {
 }
 
 // general row (origin, Dirichlet, next-to-Dirichlet rings) from the window
-__device__ __noinline__ double general_row(const LevelView& L, int b, long off,
+__device__ __forceinline__ double general_row(const LevelView& L, int b, long off,
                                               const double* __restrict__ u, int s, int t,
                                               const Coef& cP, const Coef& cTM, const Coef& cTP,
                                               const Coef& cSM, const Coef& cSP, double uP,
