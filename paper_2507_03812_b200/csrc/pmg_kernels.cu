@@ -1216,7 +1216,7 @@ __device__ __forceinline__ double general_row(const LevelView& L, int b, long of
 constexpr int kTW2 = 240;             // output nodes per strip (8 warps x 30)
 constexpr int kLn = 248;              // slot row: 242 halo nodes + alignment slack
 #ifndef PMG_TMA_LINES
-#define PMG_TMA_LINES 5
+#define PMG_TMA_LINES 4
 #endif
 #ifndef PMG_TMA_MINB
 #define PMG_TMA_MINB 2
@@ -1266,12 +1266,19 @@ inline TmaGeom tma_geom_auto(const LevelView& L) {
     return g;
 }
 
+inline long tma_min_nodes() {
+    static const long v = [] {
+        const char* e = std::getenv("PMG_TMA_MIN_NODES");
+        return e ? std::atol(e) : (4L << 20);
+    }();
+    return v;
+}
 // whether the TMA kernel applies: long lines, even n_theta (16-byte aligned
 // ring starts), and enough nodes that bandwidth, not latency, bounds the launch
 // (latency-bound small levels keep the one-tile-per-CTA kernel)
 inline bool tma_ok(const LevelView& L) {
     return L.nt >= 256 && (L.nt & 1) == 0 && L.len >= 64 && L.split >= 4 &&
-           (long)L.n * L.B >= (4L << 20);
+           (long)L.n * L.B >= tma_min_nodes();
 }
 
 // ring of node-wise row e (0 .. 6 nt): 0, 1, split-1, split, N-1, N; -1 when
