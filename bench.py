@@ -51,8 +51,10 @@ WORKLOADS = {
 }
 
 # algorithmic bytes per node of one launch
-BYTES_PER_NODE = {"residual": 56.0, "circle": 56.0, "radial": 56.0, "restrict": 10.0,
-                  "prolongate": 18.0}
+# (smooth: one zebra smoothing step = circle B+W over the circle nodes + radial
+# B+W over the radial nodes = 56 B per node of the level)
+BYTES_PER_NODE = {"residual": 56.0, "circle": 56.0, "radial": 56.0, "smooth": 56.0,
+                  "restrict": 10.0, "prolongate": 18.0}
 
 
 def env_rank():
@@ -332,19 +334,21 @@ def run_gpu(args):
     flush.add_(1.0)
     one_solve()
     breakdown = {}
-    for kind in ("residual", "circle", "radial", "restrict", "prolongate", "coarse", "norm",
-                 "other"):
+    for kind in ("residual", "smooth", "circle", "radial", "restrict", "prolongate", "coarse",
+                 "norm", "other"):
         ms, cnt = solver.profile_read(kind)
         if cnt:
             breakdown[kind] = {"ms": round(ms, 4), "launches": cnt}
     solver.profile(False)
-    dominant = max(("residual", "circle", "radial"),
+    # "smooth" = fused smoothing steps (all four zebra sweeps of a level in one
+    # launch, the latency-bound levels); circle / radial = per-colour sweeps
+    dominant = max(("residual", "smooth", "circle", "radial"),
                    key=lambda k: breakdown.get(k, {"ms": 0})["ms"])
 
     # ---- roofline of the dominant kernel on the finest level
     roof = kernel_roofline(solver, dominant, peak, peak_kind, reps=20, workload=args.workload)
     kernels = {k: kernel_roofline(solver, k, peak, peak_kind, reps=20, workload=args.workload)
-               for k in ("residual", "circle", "radial")}
+               for k in ("residual", "smooth", "circle", "radial")}
 
     if rank != 0:
         if dist:
@@ -407,7 +411,7 @@ def kernel_roofline(solver, kind, peak, peak_kind, reps=20, workload=None):
     the finest level (L2 flushed before every repetition)."""
     nr, nt, split = solver.level_shape(0)
     B = solver.n_sections
-    if kind == "residual":
+    if kind in ("residual", "smooth"):
         nodes = nr * nt
     elif kind == "circle":
         nodes = split * nt
@@ -418,7 +422,8 @@ def kernel_roofline(solver, kind, peak, peak_kind, reps=20, workload=None):
     ms = solver.time_kernel(kind, 0, reps, True)
     algo = BYTES_PER_NODE[kind] * nodes * B
     gbs = algo / (ms * 1e-3) / 1e9
-    return {"kernel": f"{kind} (finest level{', B+W' if kind != 'residual' else ''})",
+    label = {"residual": "", "smooth": ", circle B+W + radial B+W"}.get(kind, ", B+W")
+    return {"kernel": f"{kind} (finest level{label})",
             "bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
             "frac": round(gbs / peak, 4), "traffic": ncu_traffic(workload, kind),
             "ms_per_launch": round(ms, 5),

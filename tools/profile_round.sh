@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round evidence on one B200: bench lines, reference arm, ncu launch lists and
 # --set full captures of the finest-level kernels.  usage: bash tools/profile_round.sh <out>
-out=${1:-gpurun_out/r01b}
+out=${1:-gpurun_out/r01c}
 mkdir -p $out
 nvidia-smi --query-gpu=name,driver_version,clocks.max.sm,memory.total --format=csv > $out/gpu.txt
 lscpu | grep -E "Model name|^CPU\(s\)|Thread|Core" > $out/host.txt
@@ -20,7 +20,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -
     --log-file $out/levels_c1.csv python tools/solve_once.py 1 V 1 > /dev/null 2>&1
 python tools/ncu_levels.py $out/levels_c1.csv > $out/levels_c1.md
 # --set full of the finest-level kernels at 1025x1024 (first launches = level 0)
-for k in k_apply_tiled k_circle k_radial; do
+for k in k_apply_tiled k_smooth_fused; do
   ncu --set full --clock-control none --import-source on -k regex:"^${k}$" -c 2 \
       -o $out/c1_$k -f python tools/solve_once.py 1 V 1 > $out/c1_$k.log 2>&1
   python tools/ncu_summary.py $out/c1_$k.ncu-rep > $out/c1_$k.md 2>&1
