@@ -2415,6 +2415,140 @@ __global__ void __launch_bounds__(512) k_smooth_fused(LevelView L, double* __res
     }
 }
 
+
+// ------------------------------------- two-colour radial wavefront (clusters)
+// Both colours of the radial sweep of a level with clustered spokes in ONE
+// launch.  Each cluster (one spoke, C CTAs of ~862 rows) takes the next spoke
+// from a ticket counter in a host-built order in which every white spoke
+// t = 2j+1 comes `lag` black spokes after black spoke 2j+2; CTA rank r of a
+// white spoke waits for the epoch-stamped completion flags of chunks r-1..r+1
+// of black spokes t-1 and t+1 (the rows its gather reads), then gathers
+// (u through L2), solves and stamps its own chunk flag.  Black spokes wait for
+// nothing (the white spokes they read are not written before they are done).
+// A white spoke's own coefficients and its neighbours' were read by the black
+// spokes shortly before, so its gather hits L2: 72 -> ~52 B/node of DRAM
+// traffic for the B+W pair, and no kernel boundary between the colours.
+template <int K>
+__global__ void __launch_bounds__(256, PMG_CL_MINB) k_radial_wave(LevelView L, double* __restrict__ u,
+                                                     const double* __restrict__ f,
+                                                     const double* __restrict__ ril,
+                                                     const double* __restrict__ rm,
+                                                     FuseCtl fc, const int* __restrict__ order,
+                                                     int nctas) {
+    pdl_enter();
+    extern __shared__ double smem[];
+    __shared__ ClX xch;
+    __shared__ int s_t;
+    __shared__ unsigned s_ep;
+    cg::cluster_group cl = cg::this_cluster();
+    const int C = cl.num_blocks(), rank = cl.block_rank();
+    if (rank == 0 && threadIdx.x == 0) {
+        s_t = order[atomicAdd(&fc.ctl[0], 1u)];
+        s_ep = *reinterpret_cast<volatile unsigned*>(&fc.ctl[2]);
+    }
+    cl.sync();
+    const int t = *cl.map_shared_rank(&s_t, 0);
+    const unsigned ep = *cl.map_shared_rank(&s_ep, 0);
+    const int b = 0;
+    const int len = L.len, split = L.split, T = blockDim.x;
+    const int R = cl_rows(len, C), row0 = rank * R;
+    const int nloc = min(R, len - row0);
+    double* U = u;
+    const double* F = f;
+    const int base = split * L.nt + t * len;
+    const int pn = padded(R + 1);
+    double* Y = smem;
+    double* IL = smem + pn;
+    double* Mx = IL + pn;
+    double* scr = Mx + pn;
+    const long fo = ((long)b * L.nt + t) * len;
+    for (int j = threadIdx.x; j < nloc; j += T)
+        __pipeline_memcpy_async(&IL[P(j)], &ril[fo + row0 + j], 8);
+    for (int j = threadIdx.x; j <= nloc; j += T) {
+        if (row0 + j > 0)
+            __pipeline_memcpy_async(&Mx[P(j)], &rm[fo + row0 + j - 1], 8);
+        else
+            Mx[P(j)] = 0.0;
+    }
+    __pipeline_commit();
+    const int tm = L.tminus(t), tp = L.tplus(t);
+    if (t & 1) {  // white: black neighbours' chunks r-1..r+1 done
+        if (threadIdx.x < 6) {
+            const int nb = threadIdx.x < 3 ? tm : tp;
+            const int r = rank - 1 + (threadIdx.x % 3);
+            if (r >= 0 && r < C)
+                while (ld_acquire(&fc.flags[nb * C + r]) != ep) __nanosleep(64);
+        }
+        __syncthreads();
+    }
+    const double km = L.k[tm], kp = L.k[t], rkm = L.rk[tm], rkp = L.rk[t];
+    const int dTM = (tm - t) * len, dTP = (tp - t) * len;
+    const double* __restrict__ ATT = L.att;
+    const double* __restrict__ ART = L.art;
+    const int N = L.nr - 1;
+    const CoefAt<false> cf{&L, 0, b};
+#pragma unroll 2
+    for (int j = threadIdx.x; j < nloc; j += T) {
+        const int i = row0 + j, s = split + i, p = base + i;
+        double acc;
+        if (i > 0 && s < N) {
+            const double fP = F[p];
+            const double attP = ATT[p], attM = ATT[p + dTM], attQ = ATT[p + dTP];
+            const double artM = ART[p + dTM], artQ = ART[p + dTP];
+            const double artSM = ART[p - 1], artSP = ART[p + 1];
+            const double uM = ldu<true>(&U[p + dTM]), uQ = ldu<true>(&U[p + dTP]);
+            const double uMM = ldu<true>(&U[p + dTM - 1]), uQM = ldu<true>(&U[p + dTP - 1]);
+            const double uMP = ldu<true>(&U[p + dTM + 1]), uQP = ldu<true>(&U[p + dTP + 1]);
+            const double hbar = 0.5 * (L.h[s - 1] + L.h[s]);
+            const double south = -xdiv(hbar, km, rkm) * (attP + attM);
+            const double north = -xdiv(hbar, kp, rkp) * (attP + attQ);
+            acc = fP;
+            acc -= south * uM;
+            acc -= north * uQ;
+            acc -= (-(artM + artSM) * 0.25) * uMM;
+            acc -= ((artSM + artQ) * 0.25) * uQM;
+            if (s + 1 < N || !L.dir(s + 1)) {
+                acc -= ((artM + artSP) * 0.25) * uMP;
+                acc -= (-(artSP + artQ) * 0.25) * uQP;
+            }
+        } else if (L.dir(s)) {
+            acc = F[p];
+        } else {
+            const Nbr q = neighbours(L, s, t, p);
+            const Row R2 = make_row_fast(L, cf, s, t, p, q);
+            acc = F[p];
+            if (s == split && R2.has_sm) acc -= R2.sm * ldu<true>(&U[q.pSM]);
+            acc -= R2.tm * ldu<true>(&U[q.pTM]);
+            acc -= R2.tp * ldu<true>(&U[q.pTP]);
+            if (R2.has_sm) {
+                acc -= R2.mm * ldu<true>(&U[q.pSMTM]);
+                acc -= R2.mp * ldu<true>(&U[q.pSMTP]);
+            }
+            if (R2.has_sp) {
+                acc -= R2.pm * ldu<true>(&U[q.pSPTM]);
+                acc -= R2.pp * ldu<true>(&U[q.pSPTP]);
+            }
+        }
+        Y[P(j)] = acc;
+    }
+    __pipeline_wait_prior(0);
+    for (int j = threadIdx.x; j < nloc; j += T) IL[P(j)] = __drcp_rn(IL[P(j)]);
+    __syncthreads();
+    line_solve_cl<K, false>(Y, IL, Mx, nloc, row0, len, 0.0, scr, xch, len);
+    for (int j = threadIdx.x; j < nloc; j += T) U[base + row0 + j] = Y[P(j)];
+    __syncthreads();  // every thread's stores of the chunk issued
+    if (threadIdx.x == 0) {
+        __threadfence();
+        st_release(&fc.flags[t * C + rank], ep);
+        if (atomicAdd(&fc.ctl[1], 1u) == (unsigned)nctas - 1) {  // last CTA: reset
+            fc.ctl[0] = 0;
+            fc.ctl[1] = 0;
+            __threadfence();
+            atomicAdd(&fc.ctl[2], 1u);
+        }
+    }
+}
+
 // ---------------------------------------------------------------- transfers
 // restrict_transpose (interpolation.cpp:97-143) fused with
 // mask_dirichlet_rows (multigrid.cpp:146-153) and the coarse u = 0 (:204).
@@ -3695,6 +3829,53 @@ void launch_smooth_fused(const LevelView& L, bool onfly, double* u, const double
     }
 #undef PMG_FK
 #undef PMG_F
+}
+
+// Two-colour radial wavefront (k_radial_wave): cluster size when it applies
+// (one section, clustered Take spokes, fast mode, PMG_RADIAL_WAVE=1), else 0.
+// Opt-in: measured slower than the two per-colour launches (8193x8192 B+W
+// 1.35 vs 1.20 ms for lags 64-400; c2-V 23.9 vs 23.3 ms) -- the ticket
+// broadcast barrier, L2 loads of u and flag waits cost more than the
+// neighbour re-reads it saves.
+int radial_wave_cluster(const LevelView& L, bool serial, bool onfly) {
+    static const bool on = [] {
+        const char* e = std::getenv("PMG_RADIAL_WAVE");
+        return e ? std::atoi(e) != 0 : false;
+    }();
+    if (!on || serial || onfly || L.B != 1 || L.len <= 1024 || (L.nt & 1)) return 0;
+    return std::min(8, (L.len + 899) / 900);
+}
+
+// claim order: black spokes in increasing t, white spoke 2j+1 `lag` items
+// after black spoke 2j (so both its black neighbours were claimed before it)
+void radial_wave_order(int nt, int C, int* out) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int lag = std::max(1, sms * 8 / C);
+    if (const char* e = std::getenv("PMG_WAVE_LAG")) lag = std::max(1, std::atoi(e));
+    const int nb = nt / 2;
+    lag = std::min(lag, nb);
+    int k = 0;
+    for (int i = 0; i < nb; ++i) {
+        out[k++] = 2 * i;
+        if (i >= lag) out[k++] = 2 * (i - lag) + 1;
+    }
+    for (int j = nb - lag; j < nb; ++j) out[k++] = 2 * j + 1;
+}
+
+void launch_radial_wave(const LevelView& L, double* u, const double* f, const double* ril,
+                        const double* rm, const FuseCtl& fc, const int* order, cudaStream_t st) {
+    const int C = std::min(8, (L.len + 899) / 900);
+    int R, K, T;
+    size_t sm;
+    cl_shape(L.len, C, R, K, T, sm, 8);
+    const dim3 grid(L.nt * C);
+    const int nctas = L.nt * C;
+    if (K == 8)
+        launch_cluster(k_radial_wave<8>, C, grid, T, sm, st, L, u, f, ril, rm, fc, order, nctas);
+    else
+        launch_cluster(k_radial_wave<16>, C, grid, T, sm, st, L, u, f, ril, rm, fc, order, nctas);
 }
 
 void launch_restrict(const LevelView& F, const LevelView& C, const Weights& w, const double* fr,

@@ -175,6 +175,11 @@ bool fused_ok(const LevelView& L, bool serial, int exact_rings);
 // claim order of the B*(split+nt) lines (codes b*(split+nt) + c; c < split:
 // ring c, else spoke c - split)
 void fused_order(int split, int nt, int B, int* out);
+int radial_wave_cluster(const LevelView& L, bool serial, bool onfly);
+void radial_wave_order(int nt, int C, int* out);
+// both colours of a clustered radial sweep in one launch (flags [nt * C])
+void launch_radial_wave(const LevelView& L, double* u, const double* f, const double* ril,
+                        const double* rm, const FuseCtl& fc, const int* order, cudaStream_t st);
 void launch_smooth_fused(const LevelView& L, bool onfly, double* u, const double* f,
                          const double* cil, const double* cm, const double* corner,
                          const double* cz, const OriginFactor& of, const double* ril,

@@ -187,6 +187,9 @@ struct Level {
     // fused smoothing step (fused_ok levels): claim order and completion flags
     int* forder = nullptr;
     unsigned* fflags = nullptr;
+    // two-colour radial wavefront (clustered spokes): claim order and chunk flags
+    int* worder = nullptr;
+    unsigned* wflags = nullptr;
 };
 
 struct Solver {
@@ -746,6 +749,23 @@ struct Solver {
             V.forder = upload(order);
             V.fflags = alloc<unsigned>((size_t)B * per);
         }
+        for (size_t l = 0; l < lv.size(); ++l) {
+            Level& V = lv[l];
+            if (V.forder || (coarse_start >= 0 && (int)l >= coarse_start)) continue;
+            if (l == 0 && set.extrapolation) continue;
+            const int C = radial_wave_cluster(V.v, serial, onfly);
+            if (C <= 0) continue;
+            if (!fuse_ctl) {
+                fuse_ctl = alloc<unsigned>(4);
+                const unsigned init[4] = {0u, 0u, 1u, 0u};
+                PMG_CUDA(cudaMemcpyAsync(fuse_ctl, init, sizeof init, cudaMemcpyHostToDevice,
+                                         stream));
+            }
+            std::vector<int> order(V.v.nt);
+            radial_wave_order(V.v.nt, C, order.data());
+            V.worder = upload(order);
+            V.wflags = alloc<unsigned>((size_t)V.v.nt * C);
+        }
         PMG_CUDA(cudaStreamSynchronize(stream));
     }
 
@@ -1058,7 +1078,12 @@ struct Solver {
                 launch_circle(V.v, onfly, V.u, V.f, V.cil, V.cm, V.corner, V.cz, V.of(), parity,
                               serial, exact_rings, act, stream);
             });
-        if (V.v.len > 0)
+        if (V.worder) {
+            run(KK_RADIAL, 1, [&] {
+                launch_radial_wave(V.v, V.u, V.f, V.ril, V.rm, FuseCtl{fuse_ctl, V.wflags},
+                                   V.worder, stream);
+            });
+        } else if (V.v.len > 0)
             for (int parity = 0; parity < 2; ++parity)
                 run(KK_RADIAL, 1, [&] {
                     launch_radial(V.v, onfly, V.u, V.f, V.ril, V.rm, parity, serial, act, stream);
@@ -1956,6 +1981,14 @@ int pmg_time_kernel(pmg_handle h, int kind, int level, int reps, int flush_l2,
                         });
                     break;
                 case 2:
+                    if (V.worder) {  // both colours in one wavefront launch, as in smooth()
+                        s.run(pmg::KK_RADIAL, 1, [&] {
+                            pmg::launch_radial_wave(V.v, V.u, V.f, V.ril, V.rm,
+                                                    pmg::FuseCtl{s.fuse_ctl, V.wflags}, V.worder,
+                                                    s.stream);
+                        });
+                        break;
+                    }
                     for (int p = 0; p < 2; ++p)
                         s.run(pmg::KK_RADIAL, 1, [&] {
                             pmg::launch_radial(V.v, s.onfly, V.u, V.f, V.ril, V.rm, p, s.serial,
