@@ -172,3 +172,27 @@ def test_solve(pair):
     dh = np.abs(h[:k] - out["residual_norms"][:k]).max()
     sens_h = np.abs(pert["residual_norms"][:k] - out["residual_norms"][:k]).max()
     assert dh <= max(1e-12 * h[0], 4 * sens_h), (dh, sens_h)
+
+
+# Levels of >= 4M nodes take the TMA-streamed residual (k_apply_tma: strips of
+# lean rows + node-wise origin / interface / Dirichlet rings); the cases above
+# stay below that size, so the streamed kernel is pinned bitwise here on
+# 2049x2048 grids (divideBy2 route).
+TMA_CASES = {
+    "czarny2049": mk("Czarny", grid_mode=1, a=8, b=8, divide_by_2=3),
+    "shaf2049_interior": mk("Shafranov", grid_mode=1, a=8, b=8, divide_by_2=3,
+                            boundary_mode=1, R0=0.013),
+}
+
+
+@pytest.mark.parametrize("name", list(TMA_CASES))
+def test_tma_residual_bitwise(name):
+    c = TMA_CASES[name]
+    ref, gpu = Checker(c), gpu_solver(c)
+    n = ref.n(0)
+    assert n >= 4 * 2**20  # the streamed kernel's size threshold
+    rng = np.random.default_rng(41)
+    u = rng.uniform(-1, 1, n)
+    f = rng.uniform(-1, 1, n)
+    assert np.array_equal(gpu.apply(u, 0), ref.apply(u, 0, "Take"))
+    assert np.array_equal(gpu.residual(u, f, 0), ref.residual(u, f, 0, "Take"))
