@@ -72,6 +72,12 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef PMG_CL_MINB
 #define PMG_CL_MINB 4
 #endif
+// fused smoothing step: resident CTAs per SM (registers <= 65536 / (256 * MINB));
+// measured: 2 (128 regs) c1 5.71 ms, 3 (80 regs) 5.42 ms, 4 (64 regs, spills) 5.52 ms;
+// line_shape never picks more than 256 threads
+#ifndef PMG_FUSED_MINB
+#define PMG_FUSED_MINB 3
+#endif
 #ifndef PMG_ORIGIN_SCAN_MIN
 #define PMG_ORIGIN_SCAN_MIN 0
 #endif
@@ -2347,7 +2353,7 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 }
 
 template <bool ONFLY, int K>
-__global__ void __launch_bounds__(512) k_smooth_fused(LevelView L, double* __restrict__ u,
+__global__ void __launch_bounds__(256, PMG_FUSED_MINB) k_smooth_fused(LevelView L, double* __restrict__ u,
                                                       const double* __restrict__ f,
                                                       const double* __restrict__ cil,
                                                       const double* __restrict__ cm,
