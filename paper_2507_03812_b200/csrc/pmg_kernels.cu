@@ -75,6 +75,11 @@ constexpr unsigned FULL = 0xffffffffu;
 // fused smoothing step: resident CTAs per SM (registers <= 65536 / (256 * MINB));
 // measured: 2 (128 regs) c1 5.71 ms, 3 (80 regs) 5.42 ms, 4 (64 regs, spills) 5.52 ms;
 // line_shape never picks more than 256 threads
+// single-CTA line kernels with K <= 8 rows per thread run at most 256 threads
+// (line_shape); K = 16 (reference-order solves of 8192-node lines) up to 512
+#ifndef PMG_LINE_MINB
+#define PMG_LINE_MINB 3
+#endif
 #ifndef PMG_FUSED_MINB
 #define PMG_FUSED_MINB 3
 #endif
@@ -1561,7 +1566,9 @@ __global__ void __launch_bounds__(288, PMG_TMA_MINB) k_apply_tma(LevelView L, Tm
 // One circle line (ring s of section b), reference smoother.cpp:95-116,
 // 144-182: rhs gather, then the cyclic Sherman-Morrison solve
 // (line_algebra.cpp:98-120) or the envelope solve of the across-origin ring.
-template <bool ONFLY, int K, bool CG>
+// wait(): called once the line's own loads are in flight and before any u of
+// another line is read (the fused smoothing step waits for those lines there).
+template <bool ONFLY, int K, bool CG, class Wait>
 __device__ __forceinline__ void circle_body(const LevelView& L, double* __restrict__ u,
                                             const double* __restrict__ f,
                                             const double* __restrict__ cil,
@@ -1569,7 +1576,7 @@ __device__ __forceinline__ void circle_body(const LevelView& L, double* __restri
                                             const double* __restrict__ corner,
                                             const double* __restrict__ cz,
                                             const OriginFactor& of, int serial, int exact_rings,
-                                            int b, int s, double* smem) {
+                                            int b, int s, double* smem, const Wait& wait) {
     const int nt = L.nt, T = blockDim.x;
     const long off = (long)b * L.n;
     double* U = u + off;
@@ -1596,6 +1603,7 @@ __device__ __forceinline__ void circle_body(const LevelView& L, double* __restri
         __pipeline_commit();
     }
     KT(1);
+    wait();
     if (L.rows) {  // assembled rows (stencil.cpp:44-137 values, k_rows)
         const double* Rw = L.rows + (long)b * 10 * L.n;
         const int n = L.n;
@@ -1653,7 +1661,7 @@ __device__ __forceinline__ void circle_body(const LevelView& L, double* __restri
     for (int t = threadIdx.x; t < nt; t += T) U[base + t] = Y[P(t)];
     KT(5);}
 template <bool ONFLY, int K>
-__global__ void __launch_bounds__(512) k_circle(LevelView L, double* __restrict__ u,
+__global__ void __launch_bounds__(K >= 16 ? 512 : 256, K >= 16 ? 1 : PMG_LINE_MINB) k_circle(LevelView L, double* __restrict__ u,
                                                 const double* __restrict__ f,
                                                 const double* __restrict__ cil,
                                                 const double* __restrict__ cm,
@@ -1668,7 +1676,7 @@ __global__ void __launch_bounds__(512) k_circle(LevelView L, double* __restrict_
     const int b = blockIdx.y;
     if (active && !active[b]) return;
     circle_body<ONFLY, K, false>(L, u, f, cil, cm, corner, cz, of, serial, exact_rings, b,
-                                 parity + 2 * blockIdx.x, smem);
+                                 parity + 2 * blockIdx.x, smem, [] {});
 }
 
 // ------------------------------------------------------------- radial sweep
@@ -1678,12 +1686,12 @@ __global__ void __launch_bounds__(512) k_circle(LevelView L, double* __restrict_
 // an identity row.
 // One radial line (spoke t of section b), reference smoother.cpp:118-142,
 // 184-205: rhs gather, then the tridiagonal LL^T solve (line_algebra.cpp:42-62).
-template <bool ONFLY, int K, bool CG>
+template <bool ONFLY, int K, bool CG, class Wait>
 __device__ __forceinline__ void radial_body(const LevelView& L, double* __restrict__ u,
                                             const double* __restrict__ f,
                                             const double* __restrict__ ril,
                                             const double* __restrict__ rm, int serial, int b,
-                                            int t, double* smem) {
+                                            int t, double* smem, const Wait& wait) {
     const int len = L.len, split = L.split, T = blockDim.x;
     const long off = (long)b * L.n;
     double* U = u + off;
@@ -1702,6 +1710,7 @@ __device__ __forceinline__ void radial_body(const LevelView& L, double* __restri
     }
     __pipeline_commit();
     KT(1);
+    wait();
     // interior rows split < s < n_r-1 (Take): only the off-line couplings --
     // angular (att) and corner (art) -- with direct spoke-major offsets; all
     // operands of two rows are loaded before any arithmetic (memory-level
@@ -1810,7 +1819,8 @@ __global__ void __launch_bounds__(512) k_radial(LevelView L, double* __restrict_
     extern __shared__ double smem[];
     const int b = blockIdx.y;
     if (active && !active[b]) return;
-    radial_body<ONFLY, K, false>(L, u, f, ril, rm, serial, b, parity + 2 * blockIdx.x, smem);
+    radial_body<ONFLY, K, false>(L, u, f, ril, rm, serial, b, parity + 2 * blockIdx.x, smem,
+                                 [] {});
 }
 
 // ------------------------------------------------- cluster-split line solves
@@ -2379,6 +2389,8 @@ __global__ void __launch_bounds__(256, PMG_FUSED_MINB) k_smooth_fused(LevelView 
     const unsigned ep = s_epoch;
     unsigned* flags = fc.flags + (long)b * per;
     if (!active || active[b]) {
+        // the line's factors are prefetched before the wait (inside the body)
+        auto wait = [&] {
         if (threadIdx.x == 0) {
             int dep[2] = {-1, -1};
             if (c < L.split) {
@@ -2400,10 +2412,12 @@ __global__ void __launch_bounds__(256, PMG_FUSED_MINB) k_smooth_fused(LevelView 
                     while (ld_acquire(&flags[dep[d]]) != ep) __nanosleep(32);
         }
         __syncthreads();
+        };
         if (c < L.split)
-            circle_body<ONFLY, K, true>(L, u, f, cil, cm, corner, cz, of, 0, exact_rings, b, c, smem);
+            circle_body<ONFLY, K, true>(L, u, f, cil, cm, corner, cz, of, 0, exact_rings, b, c, smem,
+                                        wait);
         else
-            radial_body<ONFLY, K, true>(L, u, f, ril, rm, 0, b, c - L.split, smem);
+            radial_body<ONFLY, K, true>(L, u, f, ril, rm, 0, b, c - L.split, smem, wait);
         __syncthreads();  // every thread's stores of the line issued
         if (threadIdx.x == 0) {
             __threadfence();
