@@ -2358,6 +2358,17 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// polling load: relaxed (an acquire load compiles to a load + L1 invalidate,
+// which on every poll iteration would wipe the L1 of all CTAs on the SM);
+// the waiter issues one acquire fence after its polls succeed
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acquire() {
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -2407,9 +2418,13 @@ __global__ void __launch_bounds__(256, PMG_FUSED_MINB) k_smooth_fused(LevelView 
                     dep[0] = L.split - 1;
                 }
             }
+            bool waited = false;
             for (int d = 0; d < 2; ++d)
-                if (dep[d] >= 0)
-                    while (ld_acquire(&flags[dep[d]]) != ep) __nanosleep(32);
+                if (dep[d] >= 0) {
+                    while (ld_relaxed(&flags[dep[d]]) != ep) __nanosleep(32);
+                    waited = true;
+                }
+            if (waited) fence_acquire();
         }
         __syncthreads();
         };
@@ -2419,13 +2434,9 @@ __global__ void __launch_bounds__(256, PMG_FUSED_MINB) k_smooth_fused(LevelView 
         else
             radial_body<ONFLY, K, true>(L, u, f, ril, rm, 0, b, c - L.split, smem, wait);
         __syncthreads();  // every thread's stores of the line issued
-        if (threadIdx.x == 0) {
-            __threadfence();
-            st_release(&flags[c], ep);
-        }
+        if (threadIdx.x == 0) st_release(&flags[c], ep);  // release: orders the CTA's stores
     }
     if (threadIdx.x == 0) {
-        __threadfence();
         if (atomicAdd(&fc.ctl[1], 1u) == (unsigned)nitems - 1) {  // last CTA: reset for the next launch
             fc.ctl[0] = 0;
             fc.ctl[1] = 0;
