@@ -1,4 +1,4 @@
-out=gpurun_out/r01d
+out=${1:-gpurun_out/r01e}
 mkdir -p $out
 nvidia-smi --query-gpu=name,driver_version,clocks.max.sm,memory.total --format=csv > $out/gpu.txt
 python bench.py > $out/bench_c1.json 2> $out/bench_c1.err
