@@ -3359,9 +3359,36 @@ __global__ void __launch_bounds__(256) k_norm_partials(const double* __restrict_
 }
 
 // compute_norm (multigrid.cpp:48-59) from block partials; one block per section
+// convergence bookkeeping of section b from its residual norm r
+// (multigrid.cpp:321-340: history, r0, relative / absolute tolerance,
+// max_iterations); per section, so the norm block of b can run it
+__device__ __forceinline__ void check_section(int b, double r, const ConvState& cs, int max_it,
+                                              double rel_tol, double abs_tol) {
+    if (!cs.active[b]) return;
+    const int it = cs.count[b]++;  // residual norms taken so far = iteration index
+    if (it < cs.cap) cs.hist[(long)b * cs.cap + it] = r;
+    bool conv;
+    if (it == 0) {
+        cs.r0[b] = r;
+        conv = r == 0.0 || (abs_tol > 0.0 && r <= abs_tol);
+    } else {
+        conv = (abs_tol > 0.0 && r <= abs_tol) || (rel_tol > 0.0 && r <= rel_tol * cs.r0[b]);
+    }
+    cs.iters[b] = it;
+    if (conv) cs.converged[b] = 1;
+    if (conv || it >= max_it) {
+        cs.active[b] = 0;
+        atomicSub(cs.remaining, 1);
+    }
+}
+
+// CHECK: the block of section b also runs its convergence check (one launch
+// instead of norm + check)
+template <bool CHECK>
 __global__ void __launch_bounds__(1024) k_norm_final(const double* __restrict__ partials,
                                                      int nblk, long n, int norm_type,
-                                                     double* __restrict__ norms) {
+                                                     double* __restrict__ norms, ConvState cs,
+                                                     int max_it, double rel_tol, double abs_tol) {
     pdl_enter();
     const int b = blockIdx.x;
     const double* Pb = partials + (long)b * nblk;
@@ -3401,6 +3428,7 @@ __global__ void __launch_bounds__(1024) k_norm_final(const double* __restrict__ 
         else if (norm_type == 1)
             s = sqrt(s);
         norms[b] = s;
+        if (CHECK) check_section(b, s, cs, max_it, rel_tol, abs_tol);
     }
 }
 
@@ -3409,23 +3437,8 @@ __global__ void k_check(const double* __restrict__ norms, ConvState cs, int B, i
                         double rel_tol, double abs_tol) {
     pdl_enter();
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= B || !cs.active[b]) return;
-    const int it = cs.count[b]++;  // residual norms taken so far = iteration index
-    const double r = norms[b];
-    if (it < cs.cap) cs.hist[(long)b * cs.cap + it] = r;
-    bool conv;
-    if (it == 0) {
-        cs.r0[b] = r;
-        conv = r == 0.0 || (abs_tol > 0.0 && r <= abs_tol);
-    } else {
-        conv = (abs_tol > 0.0 && r <= abs_tol) || (rel_tol > 0.0 && r <= rel_tol * cs.r0[b]);
-    }
-    cs.iters[b] = it;
-    if (conv) cs.converged[b] = 1;
-    if (conv || it >= max_it) {
-        cs.active[b] = 0;
-        atomicSub(cs.remaining, 1);
-    }
+    if (b >= B) return;
+    check_section(b, norms[b], cs, max_it, rel_tol, abs_tol);
 }
 
 __global__ void k_fill(double* p, long n, double v) {
@@ -3939,8 +3952,15 @@ int launch_norm_partials(const double* v, long n, int B, int norm_type, double* 
 
 void launch_norm_final(const double* partials, int nblk, int B, long n, int norm_type,
                        double* norms, cudaStream_t st) {
-    launch_k(k_norm_final, B, nblk >= 4096 ? 1024 : 256, 0, st, partials, nblk, n, norm_type,
-             norms);
+    launch_k(k_norm_final<false>, B, nblk >= 4096 ? 1024 : 256, 0, st, partials, nblk, n,
+             norm_type, norms, ConvState{}, 0, 0.0, 0.0);
+}
+
+void launch_norm_check(const double* partials, int nblk, int B, long n, int norm_type,
+                       double* norms, ConvState cs, int max_it, double rel_tol, double abs_tol,
+                       cudaStream_t st) {
+    launch_k(k_norm_final<true>, B, nblk >= 4096 ? 1024 : 256, 0, st, partials, nblk, n,
+             norm_type, norms, cs, max_it, rel_tol, abs_tol);
 }
 
 void launch_check(const double* norms, ConvState cs, int B, int max_it, double rel_tol,

@@ -214,6 +214,10 @@ struct ConvState {
 };
 void launch_check(const double* norms, ConvState cs, int B, int max_it, double rel_tol,
                   double abs_tol, cudaStream_t st);
+// norm + convergence check in one launch (launch_norm_final + launch_check)
+void launch_norm_check(const double* partials, int nblk, int B, long n, int norm_type,
+                       double* norms, ConvState cs, int max_it, double rel_tol, double abs_tol,
+                       cudaStream_t st);
 
 void launch_fill(double* p, long n, double v, cudaStream_t st);
 void launch_set_active(int* active, int* count, int* conv, int* remaining, int B,

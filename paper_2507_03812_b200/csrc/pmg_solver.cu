@@ -1181,11 +1181,11 @@ struct Solver {
                                   stream);
             });
         }
-        run(KK_NORM, 2, [&] {
-            launch_norm_final(partials, nb, B, V.v.n, set.norm_type, norms, stream);
+        run(KK_NORM, 1, [&] {
             ConvState cs{r0, hist, active, iters, conv, remaining, count, hist_cap};
-            launch_check(norms, cs, B, set.max_iterations, set.relative_tolerance,
-                         set.absolute_tolerance, stream);
+            launch_norm_check(partials, nb, B, V.v.n, set.norm_type, norms, cs,
+                              set.max_iterations, set.relative_tolerance, set.absolute_tolerance,
+                              stream);
         });
     }
 
