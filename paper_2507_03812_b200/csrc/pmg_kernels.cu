@@ -3852,6 +3852,19 @@ void launch_smooth_fused(const LevelView& L, bool onfly, double* u, const double
     const int nitems = (L.split + L.nt) * L.B;
     int K, T;
     line_shape(n, K, T, nitems);
+    // Short lines (<= 256 nodes, the latency-bound coarse levels): at least 128
+    // threads per line even if some idle in the scans -- the rhs gather is the
+    // latency, and more threads put more of its loads in flight (c1: 32/64-
+    // thread lines 5.25 ms per solve, 128 threads 5.11 ms; PMG_FUSED_SMALL_T)
+    static const int small_t = [] {
+        const char* e = std::getenv("PMG_FUSED_SMALL_T");
+        return e ? std::atoi(e) : 128;
+    }();
+    if (small_t > 0 && n <= 256 && T < small_t) {
+        T = small_t;
+        K = 2;
+        while (K < 16 && K * T < n) K *= 2;
+    }
     const size_t sm = line_smem(n);
 #define PMG_F(ON, KK)                                                                          \
     do {                                                                                       \
