@@ -95,7 +95,9 @@ typedef struct {
     int max_levels;        /* 0 = coarsen as far as possible */
     int pre_smoothing, post_smoothing;
     int cycle;             /* 0 V, 1 W, 2 F */
-    int extrapolation;     /* must be 0 (not supported yet) */
+    int extrapolation;     /* 1: implicit extrapolation (multigrid.cpp:159-168,224-248); pmg_solve
+                              then assembles the manufactured RHS of levels 0 and 1 (like the
+                              reference's solve()) instead of using the RHS set by pmg_set_rhs */
     int fmg;               /* 1: full-multigrid start (multigrid.cpp:250-265); pmg_solve then
                               assembles the manufactured RHS of every level (like the
                               reference's solve()) instead of using the current f */
@@ -106,10 +108,11 @@ typedef struct {
     double relative_tolerance;  /* <= 0 disables */
     int max_threads;       /* accepted for API compatibility (host threads unused) */
     int verbose;
-    /* extension: 1 = every line solve in the reference's sequential operation
-     * order, making solves bitwise identical to the reference CPU solver
-     * (slower); 0 = chunked parallel line scans (default; the ill-conditioned
-     * across-origin ring always keeps the reference order). */
+    /* extension: 1 (default) = every line solve reproduces the reference's
+     * sequential substitution bit for bit (computed in parallel by speculation
+     * and verification), so solves are bitwise identical to the
+     * reference CPU solver; 0 = chunked parallel line scans (faster, results
+     * differ from the reference at the problem's roundoff floor). */
     int reference_order;
 } pmg_settings;
 

@@ -44,7 +44,16 @@ __device__ unsigned long long g_ktrace[32];
         if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && (slot) >= 0) \
             g_ktrace[16 + 5 * (slot) + (i)] = clock64();            \
     } while (0)
+// a value (e.g. a wave count) of thread 0 of block (0,0)
+#define KTV(i, v)                                                   \
+    do {                                                            \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) \
+            g_ktrace[i] = (v);                                      \
+    } while (0)
 #else
+#define KTV(i, v) \
+    do {          \
+    } while (0)
 #define KT(i) \
     do {      \
     } while (0)
@@ -83,6 +92,11 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef PMG_FUSED_MINB
 #define PMG_FUSED_MINB 3
 #endif
+// rows per solving thread of the exact-order parallel line solves
+#ifndef PMG_EX_CHUNK
+#define PMG_EX_CHUNK 16
+#endif
+constexpr int kExChunk = PMG_EX_CHUNK;
 #ifndef PMG_ORIGIN_SCAN_MIN
 #define PMG_ORIGIN_SCAN_MIN 0
 #endif
@@ -560,6 +574,194 @@ __device__ void tri_solve_exact(double* Y, const double* Ld, const double* M, in
     }
 }
 
+// ------------------------------------------------ exact-order parallel solve
+// Bitwise the reference's sequential substitution (tridiag_solve,
+// line_algebra.cpp:42-62, and the Sherman-Morrison step of
+// cyclic_tridiag_solve, :98-120), computed by all threads of the block:
+//  1. the chunked affine scan of the fast path gives approximate values of
+//     the iterate at every chunk boundary (a few ulps off);
+//  2. every thread restarts the reference recurrence (its operation order,
+//     division correctly rounded by Markstein's correction) one chunk early
+//     from that approximation and runs it through its own chunk.  The
+//     recurrences contract (|m/l| < 1), so after a few rows the rounding
+//     makes the restarted trajectory coincide bit for bit with the
+//     reference's;
+//  3. a chunk whose trajectory at its predecessor's last row differs from the
+//     predecessor's result is recomputed from that result, in waves, until
+//     every chunk starts from its predecessor's end bit for bit.  The result
+//     then IS the sequential substitution (induction from row 0), and every
+//     wave settles at least the first inconsistent chunk, so it terminates.
+// Y: rhs in / solution out, Ld: raw L diagonal, RC: RN(1/l), M: sub-diagonal
+// (padded shared-memory rows); z: the Sherman-Morrison vector z = T^{-1}(e_1
+// + e_n), computed at setup by the same exact sequence (k_circle_z).
+// scr: >= 64 + 3*blockDim.x doubles (line_smem(n, true) reserves 64 + 6*512).
+__device__ __forceinline__ bool same_bits(double a, double b) {
+    return __double_as_longlong(a) == __double_as_longlong(b);
+}
+// forward row j of L y = b (tridiag_solve's first loop), v = y_{j-1}.
+// Branch-free (selects, clamped indices): the rows of a chunk unroll into
+// straight-line code whose shared-memory loads the scheduler hoists ahead of
+// the dependent DMUL-DADD-DMUL-DFMA-DFMA chain.
+__device__ __forceinline__ double ex_fwd(const double* Y, const double* Ld, const double* RC,
+                                         const double* M, int j, double v) {
+    const double b = Y[P(j)];
+    const double m = M[P(j > 0 ? j - 1 : 0)];
+    const double a = b - m * v;
+    return xdiv(j == 0 ? b : a, Ld[P(j)], RC[P(j)]);
+}
+// backward row j of L^T x = y, v = x_{j+1}; yj = y_j
+__device__ __forceinline__ double ex_bwd(double yj, const double* Ld, const double* RC,
+                                         const double* M, int n, int j, double v) {
+    const double a = yj - M[P(j)] * v;
+    return xdiv(j == n - 1 ? yj : a, Ld[P(j)], RC[P(j)]);
+}
+
+// KS rows per solving thread (independent of the kernel's chunk K: threads
+// t >= ceil(n/KS) idle in the solve); warm-up = one chunk.  Each wave costs
+// one barrier: the chunk results are double-buffered.
+template <int KS, bool CYC>
+__device__ __forceinline__ void line_solve_ex(double* Y, const double* Ld, const double* RC,
+                                              const double* M, int n, double corner,
+                                              const double* __restrict__ z, double* scr) {
+    const int t = threadIdx.x, T = blockDim.x, j0 = t * KS;
+    double* Sa = scr + 64;  // approximate chunk-entry values
+    double* Se = Sa + T;    // chunk results at the chunk's far end, two buffers of T
+    const bool live = j0 < n;
+    double y[KS];
+    int waves = 0;
+    // ---- forward: y_j = (b_j - m_{j-1} y_{j-1}) / l_j  (b in Y)
+    {
+        double A = 1.0, Bv[1] = {0.0};
+#pragma unroll
+        for (int q = 0; q < KS; ++q) {
+            const int j = j0 + q;
+            if (j < n) {
+                const double il = RC[P(j)];
+                const double a = j > 0 ? -(M[P(j - 1)] * il) : 0.0;
+                Bv[0] = a * Bv[0] + Y[P(j)] * il;
+                A = a * A;
+            }
+        }
+        double yin[1];
+        block_scan<1, true>(A, Bv, yin, scr);
+        Sa[t] = yin[0];
+        __syncthreads();
+        double st = 0.0;  // this trajectory's value at row j0 - 1
+        if (live && t >= 1) {
+            double v = t >= 2 ? Sa[t - 1] : 0.0;  // thread 1 restarts at row 0: exact
+#pragma unroll
+            for (int q = 0; q < KS; ++q) v = ex_fwd(Y, Ld, RC, M, j0 - KS + q, v);
+            st = v;
+        }
+        // rows past n (last chunk) recompute row n-1 and are never stored;
+        // the chunk's far-end value is then y_{n-1} (read by no one)
+        auto chunk = [&](double v) {
+#pragma unroll
+            for (int q = 0; q < KS; ++q) {
+                const int j = min(j0 + q, n - 1);
+                const double w = ex_fwd(Y, Ld, RC, M, j, v);
+                v = j0 + q < n ? w : v;
+                y[q] = v;
+            }
+            return v;
+        };
+        double e = live ? chunk(st) : 0.0;
+        Se[t] = e;
+        __syncthreads();
+        for (int cur = 0;; cur ^= 1) {
+            const double pe = t >= 1 ? Se[cur * T + t - 1] : 0.0;
+            const bool bad = live && t >= 1 && !same_bits(st, pe);
+            if (bad) {
+                st = pe;
+                e = chunk(st);
+            }
+            Se[(cur ^ 1) * T + t] = e;
+            if (!__syncthreads_or(bad)) break;
+            ++waves;
+        }
+    }
+    // every read of b is behind the last barrier: Y now takes y
+#pragma unroll
+    for (int q = 0; q < KS; ++q)
+        if (j0 + q < n) Y[P(j0 + q)] = y[q];
+    // ---- backward: x_j = (y_j - m_j x_{j+1}) / l_j  (y in Y and in y[])
+    {
+        double G = 1.0, Dv[1] = {0.0};
+#pragma unroll
+        for (int q = KS - 1; q >= 0; --q) {
+            const int j = j0 + q;
+            if (j < n) {
+                const double il = RC[P(j)];
+                const double g = j < n - 1 ? -(M[P(j)] * il) : 0.0;
+                Dv[0] = g * Dv[0] + y[q] * il;
+                G = g * G;
+            }
+        }
+        double xin[1];
+        block_scan<1, false>(G, Dv, xin, scr);  // its barriers publish Y
+        Sa[t] = xin[0];
+        __syncthreads();
+        const bool succ = j0 + KS < n;  // a chunk follows (its rows are solved first)
+        double st = 0.0;                // this trajectory's value at row j0 + KS
+        if (live && succ) {
+            // restart one chunk late from the approximate value at row j0+2KS;
+            // if the next chunk is the last, its top row n-1 starts exactly
+            double v = j0 + 2 * KS < n ? Sa[t + 1] : 0.0;
+#pragma unroll
+            for (int q = KS - 1; q >= 0; --q) {
+                const int j = min(j0 + KS + q, n - 1);
+                const double w = ex_bwd(Y[P(j)], Ld, RC, M, n, j, v);
+                v = j0 + KS + q < n ? w : v;
+            }
+            st = v;
+        }
+        // y_j is re-read from Y (one register array per thread)
+        auto chunk = [&](double v) {
+#pragma unroll
+            for (int q = KS - 1; q >= 0; --q) {
+                const int j = min(j0 + q, n - 1);
+                const double w = ex_bwd(Y[P(j)], Ld, RC, M, n, j, v);
+                v = j0 + q < n ? w : v;
+                y[q] = v;
+            }
+            return v;
+        };
+        double e = live ? chunk(st) : 0.0;
+        Se[t] = e;
+        __syncthreads();
+        for (int cur = 0;; cur ^= 1) {
+            const double pe = t + 1 < T ? Se[cur * T + t + 1] : 0.0;
+            const bool bad = live && succ && !same_bits(st, pe);
+            if (bad) {
+                st = pe;
+                e = chunk(st);
+            }
+            Se[(cur ^ 1) * T + t] = e;
+            if (!__syncthreads_or(bad)) break;
+            waves += 1000;
+        }
+    }
+    KTV(30, waves);
+    if (CYC) {
+        // tau = c (x_0 + x_{n-1}) / (1 + c (z_0 + z_{n-1})); x -= tau z
+#pragma unroll
+        for (int q = 0; q < KS; ++q) {
+            if (j0 + q == 0) scr[0] = y[q];
+            if (j0 + q == n - 1) scr[2] = y[q];
+        }
+        __syncthreads();
+        const double tau = corner * (scr[0] + scr[2]) / (1.0 + corner * (z[0] + z[n - 1]));
+#pragma unroll
+        for (int q = 0; q < KS; ++q)
+            if (j0 + q < n) y[q] -= tau * z[j0 + q];
+    }
+    __syncthreads();  // every thread's reads of Y (and of scr) are done
+#pragma unroll
+    for (int q = 0; q < KS; ++q)
+        if (j0 + q < n) Y[P(j0 + q)] = y[q];
+    __syncthreads();
+}
+
 // Cyclic (Sherman-Morrison) solve in the reference's exact order
 // (cyclic_tridiag_solve, line_algebra.cpp:98-120).  z = T^{-1}(e_1 + e_n) is
 // rhs-independent; it was computed at setup by the same exact sequence
@@ -615,21 +817,26 @@ __device__ void origin_solve_exact(double* Y, double* B1, double* B2, const Orig
             const double y_l = ok ? Y[P(operm(i_l, h))] : 0.0;
             const double b1_l = ok ? B1[P(i_l)] : 0.0, b2_l = ok ? B2[P(i_l)] : 0.0;
             const double a1_l = ok ? r1[i_l] : 0.0, a2_l = ok ? r2[i_l] : 0.0;
-            const int cnt = nb - g < 32 ? nb - g : 32;
             double res = 0.0;
-            for (int j = 0; j < cnt; ++j) {
+            // fully unrolled, branch-free (selects): the shuffles issue ahead of
+            // the chain, which is one DMUL + DADD per row on zm1
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
                 const int i = g + j;
                 const double yv = __shfl_sync(FULL, y_l, j);
                 const double l1 = __shfl_sync(FULL, b1_l, j), l2 = __shfl_sync(FULL, b2_l, j);
                 const double a1 = __shfl_sync(FULL, a1_l, j), a2 = __shfl_sync(FULL, a2_l, j);
-                double sum = yv;
-                if (i >= 2) sum -= l2 * zm2;
-                if (i >= 1) sum -= l1 * zm1;
-                zm2 = zm1;
-                zm1 = sum;
-                if (i >= fc1) s1 -= a1 * sum;
-                if (i >= fc2) s2 -= a2 * sum;
-                if (lane == j) res = sum;
+                const double u2 = yv - l2 * zm2;
+                const double sa = i >= 2 ? u2 : yv;
+                const double u1 = sa - l1 * zm1;
+                const double sum = i >= 1 ? u1 : sa;
+                const bool valid = i < nb;
+                zm2 = valid ? zm1 : zm2;
+                zm1 = valid ? sum : zm1;
+                const double t1 = s1 - a1 * sum, t2 = s2 - a2 * sum;
+                s1 = (valid && i >= fc1) ? t1 : s1;
+                s2 = (valid && i >= fc2) ? t2 : s2;
+                res = lane == j ? sum : res;
             }
             if (ok) Y[P(operm(i_l, h))] = res;
         }
@@ -668,21 +875,457 @@ __device__ void origin_solve_exact(double* Y, double* B1, double* B2, const Orig
             const double x_l = ok ? Y[P(operm(k_l, h))] : 0.0;
             const double c2_l = (ok && k_l + 2 < nb) ? B2[P(k_l + 2)] : 0.0;
             const double c1_l = (ok && k_l + 1 < nb) ? B1[P(k_l + 1)] : 0.0;
-            const int cnt = g + 1 < 32 ? g + 1 : 32;
             double res = 0.0;
-            for (int j = 0; j < cnt; ++j) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
                 const int k = g - j;
-                double x = __shfl_sync(FULL, x_l, j);
+                const double xv = __shfl_sync(FULL, x_l, j);
                 const double l2 = __shfl_sync(FULL, c2_l, j), l1 = __shfl_sync(FULL, c1_l, j);
-                if (k + 2 < nb) x -= l2 * xp2;
-                if (k + 1 < nb) x -= l1 * xp1;
-                xp2 = xp1;
-                xp1 = x;
-                if (lane == j) res = x;
+                const double u2 = xv - l2 * xp2;
+                const double sa = k + 2 < nb ? u2 : xv;
+                const double u1 = sa - l1 * xp1;
+                const double x = k + 1 < nb ? u1 : sa;
+                const bool valid = k >= 0;
+                xp2 = valid ? xp1 : xp2;
+                xp1 = valid ? x : xp1;
+                res = lane == j ? x : res;
             }
             if (ok) Y[P(operm(k_l, h))] = res;
         }
     }
+    __syncthreads();
+}
+
+// Across-origin ring in the reference's exact order (line_algebra.cpp:211-255,
+// permutation smoother.cpp:42-46), latency-optimised: the two band
+// recurrences run on ONE thread with the operands of the next four rows
+// loaded from shared memory while the current four are computed (the
+// critical path is one DMUL + DADD per row); the dense closing rows'
+// products are formed in parallel and their two sequential sums (the
+// reference's k order) run on two warps; the diagonal scaling and the dense
+// rows' column updates are per element.  Y: rhs in NATURAL order (padded) in,
+// solution out; B1, B2, Q: padded workspaces (n).
+__device__ void origin_solve_seq(double* Y, double* B1, double* B2, double* X,
+                                 const OriginFactor& of, int b, int n) {
+    const long o = (long)b * n;
+    const double* __restrict__ r1 = of.row1 + o;
+    const double* __restrict__ r2 = of.row2 + o;
+    const double* __restrict__ D = of.D + o;
+    const int h = n / 2, nb = n - 2, T = blockDim.x, t = threadIdx.x;
+    // X: the rhs in the factor's (interleaved) order; B1, B2: the band
+    for (int i = t; i < n; i += T) {
+        X[P(i)] = Y[P(operm(i, h))];
+        B1[P(i)] = of.band1[o + i];
+        B2[P(i)] = of.band2[o + i];
+    }
+    __syncthreads();
+    KT(6);
+    if (t == 0) {  // forward band: z_i = (x_i - L(i,i-2) z_{i-2}) - L(i,i-1) z_{i-1}
+        // rows 0, 1 (no L(i,i-2); row 0 no L(i,i-1)) peeled: the main loop is
+        // straight-line, the next group's operands loaded before this group's
+        // chain (critical path DMUL + DADD per row)
+        double zm2 = X[P(0)];
+        double zm1 = X[P(1)] - B1[P(1)] * zm2;
+        X[P(1)] = zm1;
+        int i = 2;
+        if (i + 4 <= nb) {
+            double xa[4], l1a[4], l2a[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                xa[q] = X[P(i + q)];
+                l1a[q] = B1[P(i + q)];
+                l2a[q] = B2[P(i + q)];
+            }
+            for (; i + 4 <= nb; i += 4) {
+                double xb[4], l1b[4], l2b[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int k = min(i + 4 + q, nb - 1);
+                    xb[q] = X[P(k)];
+                    l1b[q] = B1[P(k)];
+                    l2b[q] = B2[P(k)];
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const double z = (xa[q] - l2a[q] * zm2) - l1a[q] * zm1;
+                    X[P(i + q)] = z;
+                    zm2 = zm1;
+                    zm1 = z;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    xa[q] = xb[q];
+                    l1a[q] = l1b[q];
+                    l2a[q] = l2b[q];
+                }
+            }
+        }
+        for (; i < nb; ++i) {
+            const double z = (X[P(i)] - B2[P(i)] * zm2) - B1[P(i)] * zm1;
+            X[P(i)] = z;
+            zm2 = zm1;
+            zm1 = z;
+        }
+    }
+    __syncthreads();
+    KT(7);
+    // dense closing rows: products in parallel (into Y and B2, free here),
+    // then the two sequential sums of the reference's k order on two warps
+    for (int k = t; k < nb; k += T) {
+        const double zk = X[P(k)];
+        Y[P(k)] = r1[k] * zk;
+        B2[P(k)] = r2[k] * zk;  // B2 is reloaded before the backward band
+    }
+    __syncthreads();
+    {
+        const int w2 = T >= 64 ? 32 : 0;
+        auto chain = [&](double s, const double* Q, int f) {
+            // -= +0 past nb is an identity; loads one batch ahead
+            double pa[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) pa[q] = f + q < nb ? Q[P(f + q)] : 0.0;
+            for (int k0 = f; k0 < nb; k0 += 8) {
+                double pb[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) pb[q] = k0 + 8 + q < nb ? Q[P(k0 + 8 + q)] : 0.0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) s -= pa[q];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) pa[q] = pb[q];
+            }
+            return s;
+        };
+        double s1 = 0.0, s2 = 0.0;
+        if (t == 0) s1 = chain(X[P(n - 2)], Y, of.fc1);
+        if (t == w2) s2 = chain(X[P(n - 1)], B2, of.fc2);
+        __syncthreads();  // every read of X[n-2], X[n-1] done
+        if (t == 0) X[P(n - 2)] = s1;
+        if (t == w2) X[P(n - 1)] = s2;
+    }
+    __syncthreads();
+    if (t == 0 && n - 2 >= of.fc2) X[P(n - 1)] -= r2[n - 2] * X[P(n - 2)];
+    __syncthreads();
+    KT(8);
+    for (int i = t; i < n; i += T) {
+        X[P(i)] /= D[i];
+        B2[P(i)] = of.band2[o + i];
+    }
+    __syncthreads();
+    if (t == 0 && n - 2 >= of.fc2) X[P(n - 2)] -= r2[n - 2] * X[P(n - 1)];
+    __syncthreads();
+    {
+        const double xn1 = X[P(n - 1)], xn2 = X[P(n - 2)];
+        for (int k = t; k < nb; k += T) {
+            double x = X[P(k)];
+            if (k >= of.fc2) x -= r2[k] * xn1;
+            if (k >= of.fc1) x -= r1[k] * xn2;
+            X[P(k)] = x;
+        }
+    }
+    __syncthreads();
+    KT(9);
+    if (t == 0) {  // backward band: x_k = (g_k - L(k+2,k) x_{k+2}) - L(k+1,k) x_{k+1}
+        // rows nb-1 (no terms) and nb-2 (no L(k+2,k)) peeled
+        double xp2 = X[P(nb - 1)];
+        double xp1 = X[P(nb - 2)] - B1[P(nb - 1)] * xp2;
+        X[P(nb - 2)] = xp1;
+        int k = nb - 3;
+        if (k - 3 >= 0) {
+            double ga[4], c1a[4], c2a[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                ga[q] = X[P(k - q)];
+                c1a[q] = B1[P(k - q + 1)];
+                c2a[q] = B2[P(k - q + 2)];
+            }
+            for (; k - 3 >= 0; k -= 4) {
+                double gb[4], c1b[4], c2b[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int kk = max(k - 4 - q, 0);
+                    gb[q] = X[P(kk)];
+                    c1b[q] = B1[P(kk + 1)];
+                    c2b[q] = B2[P(kk + 2)];
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const double x = (ga[q] - c2a[q] * xp2) - c1a[q] * xp1;
+                    X[P(k - q)] = x;
+                    xp2 = xp1;
+                    xp1 = x;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    ga[q] = gb[q];
+                    c1a[q] = c1b[q];
+                    c2a[q] = c2b[q];
+                }
+            }
+        }
+        for (; k >= 0; --k) {
+            const double x = (X[P(k)] - B2[P(k + 2)] * xp2) - B1[P(k + 1)] * xp1;
+            X[P(k)] = x;
+            xp2 = xp1;
+            xp1 = x;
+        }
+    }
+    __syncthreads();
+    KT(10);
+    for (int i = t; i < n; i += T) Y[P(operm(i, h))] = X[P(i)];
+    __syncthreads();
+}
+
+// Across-origin ring in the reference's exact order (line_algebra.cpp:211-255,
+// permutation smoother.cpp:42-46), all threads of the block: the band
+// substitutions are 2nd-order recurrences, solved like line_solve_ex -- the
+// 2x2-map scan of origin_solve gives approximate states at the chunk
+// boundaries, every thread restarts the exact recurrence one chunk early and
+// waves recompute the chunks whose entry state differs from their
+// predecessor's result bit for bit.  The two dense closing rows are
+// sequential sums in the reference's k order (two independent chains on one
+// thread); the diagonal scaling and the dense rows' column updates are per
+// element.  Y: rhs in NATURAL order (padded) in, solution out; X, B1, B2:
+// padded workspaces (the band factors are staged in B1, B2); scr: >= 64 +
+// 4 * blockDim.x doubles.
+template <int K>
+__device__ void origin_solve_ex(double* Y, double* X, double* B1, double* B2,
+                                const OriginFactor& of, int b, int n, double* scr) {
+    static_assert(K >= 2, "a chunk must hold the two rows of the recurrence state");
+    const long o = (long)b * n;
+    const double* __restrict__ gb1 = of.band1 + o;
+    const double* __restrict__ gb2 = of.band2 + o;
+    const double* __restrict__ r1 = of.row1 + o;
+    const double* __restrict__ r2 = of.row2 + o;
+    const double* __restrict__ D = of.D + o;
+    const int h = n / 2, nb = n - 2, T = blockDim.x, t = threadIdx.x;
+    const int j0 = t * K;
+    const bool live = j0 < nb;
+    double* Sa = scr + 64;   // approximate entry states (2 per thread)
+    double* Se = Sa + 2 * T;  // chunk results next to the neighbour (2 per thread, 2 buffers)
+    for (int k = t; k < n; k += T) {
+        X[P(k)] = Y[P(operm(k, h))];
+        B1[P(k)] = k < nb ? gb1[k] : 0.0;
+        B2[P(k)] = k < nb ? gb2[k] : 0.0;
+    }
+    __syncthreads();
+    KT(6);
+    double z[K];
+    int waves = 0;
+    // ---- forward band: z_i = (x_i - L(i,i-2) z_{i-2}) - L(i,i-1) z_{i-1}
+    // branch-free (selects): loads hoist ahead of the chain
+    auto fstep = [&](int i, double& zm2, double& zm1) {
+        const double x = X[P(i)], l2 = B2[P(i)], l1 = B1[P(i)];
+        const double s2 = x - l2 * zm2;
+        const double sa = i >= 2 ? s2 : x;
+        const double s1 = sa - l1 * zm1;
+        const double sum = i >= 1 ? s1 : sa;
+        zm2 = zm1;
+        zm1 = sum;
+    };
+    {
+        Map2 m = {1.0, 0.0, 0.0, 1.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+            const int i = j0 + q;
+            if (i < nb) {
+                const double l1 = i >= 1 ? B1[P(i)] : 0.0, l2 = i >= 2 ? B2[P(i)] : 0.0;
+                const Map2 mi = {0.0, 1.0, -l2, -l1, 0.0, X[P(i)]};
+                m = compose2(mi, m);
+            }
+        }
+        double a0, a1;
+        block_scan2<true>(m, a0, a1, scr);
+        Sa[2 * t] = a0;
+        Sa[2 * t + 1] = a1;
+        __syncthreads();
+        KT(7);
+        double s0 = 0.0, s1 = 0.0;  // this trajectory's (z_{j0-2}, z_{j0-1})
+        if (live && t >= 1) {
+            double zm2 = t >= 2 ? Sa[2 * (t - 1)] : 0.0, zm1 = t >= 2 ? Sa[2 * (t - 1) + 1] : 0.0;
+#pragma unroll
+            for (int q = 0; q < K; ++q) fstep(j0 - K + q, zm2, zm1);
+            s0 = zm2;
+            s1 = zm1;
+        }
+        auto chunk = [&](double zm2, double zm1) {
+#pragma unroll
+            for (int q = 0; q < K; ++q) {  // rows past nb: computed on row nb-1, not stored
+                double a = zm2, c = zm1;
+                fstep(min(j0 + q, nb - 1), a, c);
+                if (j0 + q < nb) {
+                    zm2 = a;
+                    zm1 = c;
+                }
+                z[q] = zm1;
+            }
+        };
+        auto publish = [&](int buf) {  // the chunk's last two rows (the successor's entry state)
+            Se[buf * 2 * T + 2 * t] = z[K - 2];
+            Se[buf * 2 * T + 2 * t + 1] = z[K - 1];
+        };
+        if (live) chunk(s0, s1);
+        publish(0);
+        __syncthreads();
+        for (int cur = 0;; cur ^= 1) {
+            const double* Sc = Se + cur * 2 * T;
+            const double p0 = t >= 1 ? Sc[2 * (t - 1)] : 0.0, p1 = t >= 1 ? Sc[2 * (t - 1) + 1] : 0.0;
+            const bool bad = live && t >= 1 && !(same_bits(s0, p0) && same_bits(s1, p1));
+            if (bad) {
+                s0 = p0;
+                s1 = p1;
+                chunk(s0, s1);
+            }
+            publish(cur ^ 1);
+            if (!__syncthreads_or(bad)) break;
+            ++waves;
+        }
+    }
+    KT(8);
+    KTV(28, waves);
+    waves = 0;
+#pragma unroll
+    for (int q = 0; q < K; ++q)
+        if (j0 + q < nb) X[P(j0 + q)] = z[q];
+    __syncthreads();
+    // ---- dense closing rows: sequential sums in the reference's k order;
+    // the products RN(L(i,k) z_k) are formed in parallel (into Y and W, both
+    // free here), one thread runs the two chains of subtractions
+    double* W = B2;  // reloaded before the backward band
+    for (int k = t; k < nb; k += T) {
+        const double zk = X[P(k)];
+        Y[P(k)] = r1[k] * zk;
+        W[P(k)] = r2[k] * zk;
+    }
+    __syncthreads();
+    if (t == 0) {
+        // subtracting +0 is an identity, so rows outside [fc, nb) subtract 0
+        double s1 = X[P(n - 2)], s2 = X[P(n - 1)];
+        const int f1 = of.fc1, f2 = of.fc2;
+        for (int k0 = min(f1, f2); k0 < nb; k0 += 8) {
+            double p1[8], p2[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int k = k0 + q;
+                p1[q] = (k < nb && k >= f1) ? Y[P(k)] : 0.0;
+                p2[q] = (k < nb && k >= f2) ? W[P(k)] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                s1 -= p1[q];
+                s2 -= p2[q];
+            }
+        }
+        if (n - 2 >= f2) s2 -= r2[n - 2] * s1;
+        X[P(n - 2)] = s1;
+        X[P(n - 1)] = s2;
+    }
+    __syncthreads();
+    KT(9);
+    // ---- diagonal, then the dense rows' column updates (row n-1 first)
+    for (int k = t; k < n; k += T) {
+        X[P(k)] /= D[k];
+        B2[P(k)] = k < nb ? gb2[k] : 0.0;
+    }
+    __syncthreads();
+    if (t == 0 && n - 2 >= of.fc2) X[P(n - 2)] -= r2[n - 2] * X[P(n - 1)];
+    __syncthreads();
+    {
+        const double xn1 = X[P(n - 1)], xn2 = X[P(n - 2)];
+        for (int k = t; k < nb; k += T) {
+            double x = X[P(k)];
+            if (k >= of.fc2) x -= r2[k] * xn1;
+            if (k >= of.fc1) x -= r1[k] * xn2;
+            X[P(k)] = x;
+        }
+    }
+    __syncthreads();
+    KT(10);
+    // ---- backward band: x_k = (g_k - L(k+2,k) x_{k+2}) - L(k+1,k) x_{k+1}
+    auto bstep = [&](int k, double& xp1, double& xp2) {
+        const double g = X[P(k)];
+        const double l2 = B2[P(k + 2 < nb ? k + 2 : 0)], l1 = B1[P(k + 1 < nb ? k + 1 : 0)];
+        const double s2 = g - l2 * xp2;
+        const double sa = k + 2 < nb ? s2 : g;
+        const double s1 = sa - l1 * xp1;
+        const double x = k + 1 < nb ? s1 : sa;
+        xp2 = xp1;
+        xp1 = x;
+    };
+    {
+        Map2 g = {1.0, 0.0, 0.0, 1.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = K - 1; q >= 0; --q) {
+            const int k = j0 + q;
+            if (k < nb) {
+                const double l1 = k + 1 < nb ? B1[P(k + 1)] : 0.0;
+                const double l2 = k + 2 < nb ? B2[P(k + 2)] : 0.0;
+                const Map2 mk = {-l1, -l2, 1.0, 0.0, X[P(k)], 0.0};
+                g = compose2(mk, g);
+            }
+        }
+        double a0, a1;
+        block_scan2<false>(g, a0, a1, scr);  // entry state (x_{j0+K}, x_{j0+K+1})
+        Sa[2 * t] = a0;
+        Sa[2 * t + 1] = a1;
+        __syncthreads();
+        const bool succ = j0 + K < nb;
+        double s0 = 0.0, s1 = 0.0;  // this trajectory's (x_{j0+K}, x_{j0+K+1})
+        if (live && succ) {
+            double xp1 = j0 + 2 * K < nb ? Sa[2 * (t + 1)] : 0.0;
+            double xp2 = j0 + 2 * K < nb ? Sa[2 * (t + 1) + 1] : 0.0;
+#pragma unroll
+            for (int q = K - 1; q >= 0; --q) {
+                double a = xp1, c = xp2;
+                bstep(min(j0 + K + q, nb - 1), a, c);
+                if (j0 + K + q < nb) {
+                    xp1 = a;
+                    xp2 = c;
+                }
+            }
+            s0 = xp1;
+            s1 = xp2;
+        }
+        auto chunk = [&](double xp1, double xp2) {
+#pragma unroll
+            for (int q = K - 1; q >= 0; --q) {
+                double a = xp1, c = xp2;
+                bstep(min(j0 + q, nb - 1), a, c);
+                if (j0 + q < nb) {
+                    xp1 = a;
+                    xp2 = c;
+                }
+                z[q] = xp1;
+            }
+        };
+        auto publish = [&](int buf) {  // the chunk's first two rows (the predecessor's entry state)
+            Se[buf * 2 * T + 2 * t] = z[0];
+            Se[buf * 2 * T + 2 * t + 1] = z[1];
+        };
+        if (live) chunk(s0, s1);
+        publish(0);
+        __syncthreads();
+        for (int cur = 0;; cur ^= 1) {
+            const double* Sc = Se + cur * 2 * T;
+            const double p0 = t + 1 < T ? Sc[2 * (t + 1)] : 0.0;
+            const double p1 = t + 1 < T ? Sc[2 * (t + 1) + 1] : 0.0;
+            const bool bad = live && succ && !(same_bits(s0, p0) && same_bits(s1, p1));
+            if (bad) {
+                s0 = p0;
+                s1 = p1;
+                chunk(s0, s1);
+            }
+            publish(cur ^ 1);
+            if (!__syncthreads_or(bad)) break;
+            ++waves;
+        }
+    }
+    KT(11);
+    KTV(29, waves);
+#pragma unroll
+    for (int q = 0; q < K; ++q)
+        if (j0 + q < nb) X[P(j0 + q)] = z[q];
+    __syncthreads();
+    for (int k = t; k < n; k += T) Y[P(operm(k, h))] = X[P(k)];
     __syncthreads();
 }
 
@@ -1587,10 +2230,14 @@ __device__ __forceinline__ void circle_body(const LevelView& L, double* __restri
         return;
     }
     const int pn = padded(nt);
+    // serial: 0 fast (chunked scans), 1 exact order in parallel (line_solve_ex),
+    // 2 exact order on one thread (lines whose 4 shared arrays do not fit)
+    const bool par_ex = serial == 1 || (serial == 0 && exact_rings > 0);
     double* Y = smem;
     double* IL = smem + pn;
     double* M = IL + pn;
-    double* scr = M + pn;
+    double* RC = M + pn;  // RN(1/l) (par_ex only)
+    double* scr = par_ex ? RC + pn : RC;
     const CoefAt<ONFLY> cf{&L, off, b};
     const bool origin = s == 0 && L.boundary == 0;
     const long fo = (long)b * L.split * nt + (long)s * nt;
@@ -1642,7 +2289,11 @@ __device__ __forceinline__ void circle_body(const LevelView& L, double* __restri
     KT(2);
     if (origin) {
         __syncthreads();
-        if (serial || nt < PMG_ORIGIN_SCAN_MIN)
+        if (serial == 1)
+            origin_solve_seq(Y, IL, M, RC, of, b, nt);
+        else if (serial)
+            origin_solve_exact(Y, IL, M, of, b, nt);
+        else if (nt < PMG_ORIGIN_SCAN_MIN)
             origin_solve_exact(Y, IL, M, of, b, nt);
         else
             origin_solve<K>(Y, IL, of, b, nt, scr);
@@ -1650,9 +2301,13 @@ __device__ __forceinline__ void circle_body(const LevelView& L, double* __restri
         __pipeline_wait_prior(0);
         if (!exact)  // each thread converts the elements it copied
             for (int t = threadIdx.x; t < nt; t += T) IL[P(t)] = __drcp_rn(IL[P(t)]);
+        else if (par_ex)
+            for (int t = threadIdx.x; t < nt; t += T) RC[P(t)] = __drcp_rn(IL[P(t)]);
         __syncthreads();
         KT(3);
-        if (exact)
+        if (exact && par_ex)
+            line_solve_ex<kExChunk, true>(Y, IL, RC, M, nt, corner[(long)b * L.split + s], cz + fo, scr);
+        else if (exact)
             cyc_solve_exact(Y, IL, M, nt, corner[(long)b * L.split + s], cz + fo, scr);
         else
             line_solve<K, true>(Y, IL, M, nt, corner[(long)b * L.split + s], scr);
@@ -1701,7 +2356,8 @@ __device__ __forceinline__ void radial_body(const LevelView& L, double* __restri
     double* Y = smem;
     double* IL = smem + pn;
     double* M = IL + pn;
-    double* scr = M + pn;
+    double* RC = M + pn;  // RN(1/l) (serial == 1 only)
+    double* scr = serial == 1 ? RC + pn : RC;
     const CoefAt<ONFLY> cf{&L, off, b};
     const long fo = ((long)b * L.nt + t) * len;
     for (int i = threadIdx.x; i < len; i += T) {  // overlapped with the rhs
@@ -1796,10 +2452,14 @@ __device__ __forceinline__ void radial_body(const LevelView& L, double* __restri
     __pipeline_wait_prior(0);
     if (!serial)  // each thread converts the factor elements it copied
         for (int i = threadIdx.x; i < len; i += T) IL[P(i)] = __drcp_rn(IL[P(i)]);
+    else if (serial == 1)
+        for (int i = threadIdx.x; i < len; i += T) RC[P(i)] = __drcp_rn(IL[P(i)]);
     KT(2);
     __syncthreads();
     KT(3);
-    if (serial) {
+    if (serial == 1) {
+        line_solve_ex<kExChunk, false>(Y, IL, RC, M, len, 0.0, nullptr, scr);
+    } else if (serial) {
         if (threadIdx.x == 0) tri_solve_exact(Y, IL, M, len);
         __syncthreads();
     } else {
@@ -2383,7 +3043,7 @@ __global__ void __launch_bounds__(256, PMG_FUSED_MINB) k_smooth_fused(LevelView 
                                                       OriginFactor of,
                                                       const double* __restrict__ ril,
                                                       const double* __restrict__ rm,
-                                                      int exact_rings, FuseCtl fc,
+                                                      int exact_rings, int ex, FuseCtl fc,
                                                       const int* __restrict__ order, int nitems,
                                                       const int* __restrict__ active) {
     pdl_enter();
@@ -2429,10 +3089,10 @@ __global__ void __launch_bounds__(256, PMG_FUSED_MINB) k_smooth_fused(LevelView 
         __syncthreads();
         };
         if (c < L.split)
-            circle_body<ONFLY, K, true>(L, u, f, cil, cm, corner, cz, of, 0, exact_rings, b, c, smem,
-                                        wait);
+            circle_body<ONFLY, K, true>(L, u, f, cil, cm, corner, cz, of, ex, exact_rings, b, c,
+                                        smem, wait);
         else
-            radial_body<ONFLY, K, true>(L, u, f, ril, rm, 0, b, c - L.split, smem, wait);
+            radial_body<ONFLY, K, true>(L, u, f, ril, rm, ex, b, c - L.split, smem, wait);
         __syncthreads();  // every thread's stores of the line issued
         if (threadIdx.x == 0) st_release(&flags[c], ep);  // release: orders the CTA's stores
     }
@@ -2850,6 +3510,235 @@ __device__ __forceinline__ void warp_line_solve(double (&y)[KW], const double* _
     }
 }
 
+// Warp version of line_solve_ex: the reference's exact substitution order
+// (line_algebra.cpp:42-62, 98-120) by speculation within one warp -- lane l
+// restarts the recurrence over lane l-1's rows from the warp scan's
+// approximate value, then waves (ballots, no block barriers) recompute the
+// lanes whose start differs from their predecessor's result bit for bit.
+// y[]: the lane's rows [lane*KE, +KE) of the rhs on entry, the solution on
+// exit; Ld / Mo: raw L diagonal / sub-diagonal; z: exact Sherman-Morrison
+// vector (CYC).
+template <bool CYC, int KW>
+__device__ __forceinline__ void warp_line_solve_ex(double (&y)[KW], const double* __restrict__ Ld,
+                                                   const double* __restrict__ Mo, int n,
+                                                   double corner, const double* __restrict__ z) {
+    const int KE = (n + 31) >> 5;  // rows per lane (<= KW)
+    const int lane = threadIdx.x & 31, j0 = lane * KE;
+    const bool live = j0 < n;
+    double b[KW];
+#pragma unroll
+    for (int q = 0; q < KW; ++q) b[q] = y[q];
+    auto row_in = [&](int q, int j) { return q < KE && j < n; };
+    // forward: y_j = (b_j - m_{j-1} y_{j-1}) / l_j
+    double A = 1.0, Bv[1] = {0.0};
+#pragma unroll
+    for (int q = 0; q < KW; ++q) {
+        const int j = j0 + q;
+        if (row_in(q, j)) {
+            const double il = __drcp_rn(Ld[j]);
+            const double a = j > 0 ? -(Mo[j - 1] * il) : 0.0;
+            Bv[0] = a * Bv[0] + b[q] * il;
+            A = a * A;
+        }
+    }
+    double yin[1];
+    warp_scan<1, true>(A, Bv, yin);
+    auto fstep = [&](double bj, int j, double v) {
+        const double l = Ld[j];
+        return xdiv(j == 0 ? bj : bj - Mo[j - 1] * v, l, __drcp_rn(l));
+    };
+    double st;
+    {
+        double v = __shfl_up_sync(FULL, yin[0], 1);  // approximate value at row j0 - KE - 1
+#pragma unroll
+        for (int q = 0; q < KW; ++q) {
+            const double bp = __shfl_up_sync(FULL, b[q], 1);
+            const int j = j0 - KE + q;
+            if (lane >= 1 && live && q < KE) v = fstep(bp, j, v);
+        }
+        st = v;
+    }
+    auto fchunk = [&](double v) {
+#pragma unroll
+        for (int q = 0; q < KW; ++q) {
+            const int j = j0 + q;
+            if (row_in(q, j)) {
+                v = fstep(b[q], j, v);
+                y[q] = v;
+            }
+        }
+        return v;
+    };
+    double e = live ? fchunk(st) : 0.0;
+    for (;;) {
+        const double pe = __shfl_up_sync(FULL, e, 1);
+        const bool bad = lane >= 1 && live && !same_bits(st, pe);
+        if (!__any_sync(FULL, bad)) break;
+        if (bad) {
+            st = pe;
+            e = fchunk(st);
+        }
+    }
+    // backward: x_j = (y_j - m_j x_{j+1}) / l_j
+#pragma unroll
+    for (int q = 0; q < KW; ++q) b[q] = y[q];
+    double G = 1.0, Dv[1] = {0.0};
+#pragma unroll
+    for (int q = KW - 1; q >= 0; --q) {
+        const int j = j0 + q;
+        if (row_in(q, j)) {
+            const double il = __drcp_rn(Ld[j]);
+            const double g = j < n - 1 ? -(Mo[j] * il) : 0.0;
+            Dv[0] = g * Dv[0] + b[q] * il;
+            G = g * G;
+        }
+    }
+    double xin[1];
+    warp_scan<1, false>(G, Dv, xin);
+    auto bstep = [&](double yj, int j, double v) {
+        const double l = Ld[j];
+        return xdiv(j == n - 1 ? yj : yj - Mo[j] * v, l, __drcp_rn(l));
+    };
+    const bool succ = j0 + KE < n;
+    {
+        // approximate value at row j0 + 2 KE (lane + 1's entry); exact start
+        // when lane + 1 holds row n - 1
+        double v = __shfl_down_sync(FULL, xin[0], 1);
+#pragma unroll
+        for (int q = KW - 1; q >= 0; --q) {
+            const double yn = __shfl_down_sync(FULL, b[q], 1);
+            const int j = j0 + KE + q;
+            if (succ && q < KE && j < n) v = bstep(yn, j, v);
+        }
+        st = v;
+    }
+    auto bchunk = [&](double v) {
+#pragma unroll
+        for (int q = KW - 1; q >= 0; --q) {
+            const int j = j0 + q;
+            if (row_in(q, j)) {
+                v = bstep(b[q], j, v);
+                y[q] = v;
+            }
+        }
+        return v;
+    };
+    e = live ? bchunk(st) : 0.0;
+    for (;;) {
+        const double pe = __shfl_down_sync(FULL, e, 1);
+        const bool bad = live && succ && !same_bits(st, pe);
+        if (!__any_sync(FULL, bad)) break;
+        if (bad) {
+            st = pe;
+            e = bchunk(st);
+        }
+    }
+    if (CYC) {
+        const int last = (n - 1) / KE, ql = (n - 1) - last * KE;
+        double xl = 0.0;
+#pragma unroll
+        for (int q = 0; q < KW; ++q)
+            if (q == ql) xl = y[q];
+        const double x0 = __shfl_sync(FULL, y[0], 0);
+        xl = __shfl_sync(FULL, xl, last);
+        const double tau = corner * (x0 + xl) / (1.0 + corner * (z[0] + z[n - 1]));
+#pragma unroll
+        for (int q = 0; q < KW; ++q)
+            if (row_in(q, j0 + q)) y[q] -= tau * z[j0 + q];
+    }
+}
+
+// Across-origin ring of a tail level in the reference's exact order
+// (line_algebra.cpp:211-255 with the interleaved permutation of
+// smoother.cpp:42-46), one warp, in place on ring 0 of U (natural order):
+// the two recurrence chains run redundantly on every lane with the operands
+// of 32 rows preloaded and broadcast by shuffles; diagonal scaling and the
+// dense rows' column updates are per element.
+__device__ void origin_exact_warp(double* X, const OriginFactor& of, int b, int n) {
+    const long o = (long)b * n;
+    const double* __restrict__ b1 = of.band1 + o;
+    const double* __restrict__ b2 = of.band2 + o;
+    const double* __restrict__ r1 = of.row1 + o;
+    const double* __restrict__ r2 = of.row2 + o;
+    const double* __restrict__ D = of.D + o;
+    const int h = n / 2, nb = n - 2, lane = threadIdx.x & 31;
+    {
+        const int fc1 = of.fc1, fc2 = of.fc2;
+        double zm2 = 0.0, zm1 = 0.0;
+        double s1 = X[operm(n - 2, h)], s2 = X[operm(n - 1, h)];
+        for (int g = 0; g < nb; g += 32) {
+            const int i_l = g + lane;
+            const bool ok = i_l < nb;
+            const double y_l = ok ? X[operm(i_l, h)] : 0.0;
+            const double b1_l = ok ? b1[i_l] : 0.0, b2_l = ok ? b2[i_l] : 0.0;
+            const double a1_l = ok ? r1[i_l] : 0.0, a2_l = ok ? r2[i_l] : 0.0;
+            const int cnt = nb - g < 32 ? nb - g : 32;
+            double res = 0.0;
+            for (int j = 0; j < cnt; ++j) {
+                const int i = g + j;
+                const double yv = __shfl_sync(FULL, y_l, j);
+                const double l1 = __shfl_sync(FULL, b1_l, j), l2 = __shfl_sync(FULL, b2_l, j);
+                const double a1 = __shfl_sync(FULL, a1_l, j), a2 = __shfl_sync(FULL, a2_l, j);
+                double sum = yv;
+                if (i >= 2) sum -= l2 * zm2;
+                if (i >= 1) sum -= l1 * zm1;
+                zm2 = zm1;
+                zm1 = sum;
+                if (i >= fc1) s1 -= a1 * sum;
+                if (i >= fc2) s2 -= a2 * sum;
+                if (lane == j) res = sum;
+            }
+            __syncwarp();
+            if (ok) X[operm(i_l, h)] = res;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            if (n - 2 >= fc2) s2 -= r2[n - 2] * s1;
+            X[operm(n - 2, h)] = s1;
+            X[operm(n - 1, h)] = s2;
+        }
+    }
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) X[operm(i, h)] /= D[i];
+    __syncwarp();
+    if (lane == 0 && n - 2 >= of.fc2) X[operm(n - 2, h)] -= r2[n - 2] * X[operm(n - 1, h)];
+    __syncwarp();
+    {
+        const double xn1 = X[operm(n - 1, h)], xn2 = X[operm(n - 2, h)];
+        for (int k = lane; k < nb; k += 32) {
+            double x = X[operm(k, h)];
+            if (k >= of.fc2) x -= r2[k] * xn1;
+            if (k >= of.fc1) x -= r1[k] * xn2;
+            X[operm(k, h)] = x;
+        }
+    }
+    __syncwarp();
+    {
+        double xp1 = 0.0, xp2 = 0.0;  // x_{k+1}, x_{k+2}
+        for (int g = nb - 1; g >= 0; g -= 32) {
+            const int k_l = g - lane;
+            const bool ok = k_l >= 0;
+            const double x_l = ok ? X[operm(k_l, h)] : 0.0;
+            const double c2_l = (ok && k_l + 2 < nb) ? b2[k_l + 2] : 0.0;
+            const double c1_l = (ok && k_l + 1 < nb) ? b1[k_l + 1] : 0.0;
+            const int cnt = g + 1 < 32 ? g + 1 : 32;
+            double res = 0.0;
+            for (int j = 0; j < cnt; ++j) {
+                const int k = g - j;
+                double x = __shfl_sync(FULL, x_l, j);
+                const double l2 = __shfl_sync(FULL, c2_l, j), l1 = __shfl_sync(FULL, c1_l, j);
+                if (k + 2 < nb) x -= l2 * xp2;
+                if (k + 1 < nb) x -= l1 * xp1;
+                xp2 = xp1;
+                xp1 = x;
+                if (lane == j) res = x;
+            }
+            __syncwarp();
+            if (ok) X[operm(k_l, h)] = res;
+        }
+    }
+    __syncwarp();
+}
 
 // The coarse tail evaluates the assembled rows of launch_rows (Rw = this
 // section's [10][n] block): absent couplings are stored as 0 and their
@@ -3055,9 +3944,22 @@ __device__ void coarse_smooth(const CoarseLevel& C, int b, const Team& team) {
                 continue;
             }
             if (s == 0 && L.boundary == 0) {
-#ifndef PMG_EXP_NO_ORIGIN
-                origin_warp<KW, CG>(C, U, F, off, b);
-#endif
+                if (C.exact) {  // rhs into ring 0 of U, then the exact substitution in place
+                    double rr[KW];
+#pragma unroll
+                    for (int q = 0; q < KW; ++q) {
+                        const int t = lane + 32 * q;
+                        rr[q] = t < nt ? circle_rhs<CG>(L, Rw, U, F, 0, t) : 0.0;
+                    }
+                    __syncwarp();
+#pragma unroll
+                    for (int q = 0; q < KW; ++q)
+                        if (lane + 32 * q < nt) U[lane + 32 * q] = rr[q];
+                    __syncwarp();
+                    origin_exact_warp(U, C.of, b, nt);
+                } else {
+                    origin_warp<KW, CG>(C, U, F, off, b);
+                }
                 continue;
             }
             double y[KW];
@@ -3070,7 +3972,12 @@ __device__ void coarse_smooth(const CoarseLevel& C, int b, const Team& team) {
 #ifdef PMG_KTRACE
             if (kslot == 1 && parity == 1 && threadIdx.x == 0 && blockIdx.x == 0) g_ktrace[0] = clock64();
 #endif
-            warp_line_solve<true, KW>(y, C.cl + fo, C.cm + fo, nt, C.corner[(long)b * L.split + s]);
+            if (C.exact)
+                warp_line_solve_ex<true, KW>(y, C.cl + fo, C.cm + fo, nt,
+                                             C.corner[(long)b * L.split + s], C.cz + fo);
+            else
+                warp_line_solve<true, KW>(y, C.cl + fo, C.cm + fo, nt,
+                                          C.corner[(long)b * L.split + s]);
 #ifdef PMG_KTRACE
             if (kslot == 1 && parity == 1 && threadIdx.x == 0 && blockIdx.x == 0) g_ktrace[1] = clock64();
 #endif
@@ -3111,7 +4018,10 @@ __device__ void coarse_smooth(const CoarseLevel& C, int b, const Team& team) {
                 y[q] = acc;
             }
             const long fo = ((long)b * nt + t) * L.len;
-            warp_line_solve<false, KW>(y, C.rl + fo, C.rm + fo, L.len, 0.0);
+            if (C.exact)
+                warp_line_solve_ex<false, KW>(y, C.rl + fo, C.rm + fo, L.len, 0.0, nullptr);
+            else
+                warp_line_solve<false, KW>(y, C.rl + fo, C.rm + fo, L.len, 0.0);
             __syncwarp();
 #pragma unroll
             for (int q = 0; q < KW; ++q)
@@ -3511,7 +4421,15 @@ inline void line_shape(int n, int& K, int& T, long lines_total = 0) {
     if (T < 32) T = 32;
 }
 
-inline size_t line_smem(int n) { return (size_t)(3 * padded(n) + 32 * 6 + 16) * sizeof(double); }
+// shared memory of a single-CTA line: Y, IL, M (+ RC and the chunk tables of
+// the exact-order parallel solve when ex4)
+inline size_t line_smem(int n, bool ex4 = false, int T = 512) {
+    return ex4 ? (size_t)(4 * padded(n) + 64 + 6 * T) * sizeof(double)
+               : (size_t)(3 * padded(n) + 32 * 6 + 16) * sizeof(double);
+}
+// line-solve mode of an exact (reference_order) solve: 1 = parallel exact
+// (line_solve_ex) when its four line arrays fit one CTA, else 2 = one thread
+inline int exact_mode(int n) { return line_smem(n, true) <= 227 * 1024 ? 1 : 2; }
 
 }  // namespace
 
@@ -3609,10 +4527,11 @@ static void circle_k(const LevelView& L, double* u, const double* f, const doubl
                      const double* cm, const double* corner, const double* cz,
                      const OriginFactor& of, int parity, bool serial, int exact_rings,
                      const int* active, cudaStream_t st, int T, int lines) {
-    const size_t sm = line_smem(L.nt);
+    const int mode = serial ? exact_mode(L.nt) : 0;
+    const size_t sm = line_smem(L.nt, mode == 1 || (mode == 0 && exact_rings > 0), T);
     set_smem(k_circle<ON, K>, sm);
     launch_k(k_circle<ON, K>, dim3(lines, L.B), T, sm, st, L, u, f, cil, cm, corner, cz, of, parity,
-                                                      serial ? 1 : 0, exact_rings, active);
+             mode, exact_rings, active);
 }
 
 // cluster size for a line of n rows in fast mode (1 = single-CTA kernels)
@@ -3767,10 +4686,10 @@ template <bool ON, int K>
 static void radial_k(const LevelView& L, double* u, const double* f, const double* ril,
                      const double* rm, int parity, bool serial, const int* active,
                      cudaStream_t st, int T, int lines) {
-    const size_t sm = line_smem(L.len);
+    const int mode = serial ? exact_mode(L.len) : 0;
+    const size_t sm = line_smem(L.len, mode == 1, T);
     set_smem(k_radial<ON, K>, sm);
-    launch_k(k_radial<ON, K>, dim3(lines, L.B), T, sm, st, L, u, f, ril, rm, parity, serial ? 1 : 0,
-                                                      active);
+    launch_k(k_radial<ON, K>, dim3(lines, L.B), T, sm, st, L, u, f, ril, rm, parity, mode, active);
 }
 
 void launch_radial(const LevelView& L, bool onfly, double* u, const double* f, const double* ril,
@@ -3821,7 +4740,8 @@ bool fused_ok(const LevelView& L, bool serial, int exact_rings) {
         const char* e = std::getenv("PMG_FUSED_SMOOTH");
         return e ? std::atoi(e) != 0 : true;
     }();
-    return on && !serial && exact_rings <= 0 && L.len > 1 && L.split >= 2 && L.nt <= 1024 &&
+    (void)serial;
+    return on && exact_rings <= 0 && L.len > 1 && L.split >= 2 && L.nt <= 1024 &&
            L.len <= 1024 && (L.nt & 1) == 0;
 }
 
@@ -3846,8 +4766,8 @@ void fused_order(int split, int nt, int B, int* out) {
 void launch_smooth_fused(const LevelView& L, bool onfly, double* u, const double* f,
                          const double* cil, const double* cm, const double* corner,
                          const double* cz, const OriginFactor& of, const double* ril,
-                         const double* rm, int exact_rings, const FuseCtl& fc, const int* order,
-                         const int* active, cudaStream_t st) {
+                         const double* rm, int exact_rings, bool serial, const FuseCtl& fc,
+                         const int* order, const int* active, cudaStream_t st) {
     const int n = std::max(L.nt, L.len);
     const int nitems = (L.split + L.nt) * L.B;
     int K, T;
@@ -3865,12 +4785,13 @@ void launch_smooth_fused(const LevelView& L, bool onfly, double* u, const double
         K = 2;
         while (K < 16 && K * T < n) K *= 2;
     }
-    const size_t sm = line_smem(n);
+    const int ex = serial ? 1 : 0;  // lines <= 1024: the parallel exact solve always fits
+    const size_t sm = line_smem(n, serial, T);
 #define PMG_F(ON, KK)                                                                          \
     do {                                                                                       \
         set_smem(k_smooth_fused<ON, KK>, sm);                                                  \
         launch_k(k_smooth_fused<ON, KK>, dim3(nitems), T, sm, st, L, u, f, cil, cm, corner, cz, \
-                 of, ril, rm, exact_rings, fc, order, nitems, active);                         \
+                 of, ril, rm, exact_rings, ex, fc, order, nitems, active);                     \
     } while (0)
 #define PMG_FK(ON)                       \
     switch (K) {                         \
@@ -4002,6 +4923,10 @@ void launch_flush(double* buf, long n, cudaStream_t st) {
 namespace pmg {
 #ifdef PMG_KTRACE
 void read_ktrace(unsigned long long* out) { cudaMemcpyFromSymbol(out, g_ktrace, sizeof(g_ktrace)); }  // 32 entries
+void reset_ktrace() {
+    static const unsigned long long zero[32] = {};
+    cudaMemcpyToSymbol(g_ktrace, zero, sizeof(zero));
+}
 #endif
 
 void launch_mid_cycle(const MidParams& mp, const int* prog, int nops, int B, const int* active,

@@ -46,8 +46,10 @@ struct CoarseLevel {
     const double *cl, *cm, *corner;  // circle factors [B][split*nt], corner [B][split]
     const double *rl, *rm;           // radial factors [B][nt*len]
     const double* rows;              // assembled rows [B][10][n] (launch_rows)
+    const double* cz;                // Sherman-Morrison vectors [B][split*nt] (exact mode)
     OriginFactor of;
     Weights w;  // this level as the fine level of a transfer
+    int exact;  // reference-order (bitwise) line solves
 };
 
 enum CoarseOp {
@@ -113,6 +115,7 @@ struct MidParams {
 };
 #ifdef PMG_KTRACE
 void read_ktrace(unsigned long long* out);  // diagnostics build only
+void reset_ktrace();                       // diagnostics build only
 #endif
 void launch_mid_cycle(const MidParams& mp, const int* prog, int nops, int B, const int* active,
                       cudaStream_t st);
@@ -183,8 +186,8 @@ void launch_radial_wave(const LevelView& L, double* u, const double* f, const do
 void launch_smooth_fused(const LevelView& L, bool onfly, double* u, const double* f,
                          const double* cil, const double* cm, const double* corner,
                          const double* cz, const OriginFactor& of, const double* ril,
-                         const double* rm, int exact_rings, const FuseCtl& fc, const int* order,
-                         const int* active, cudaStream_t st);
+                         const double* rm, int exact_rings, bool serial, const FuseCtl& fc,
+                         const int* order, const int* active, cudaStream_t st);
 
 // mask: zero the coarse Dirichlet rows (mask_dirichlet_rows, multigrid.cpp:146-153)
 void launch_restrict(const LevelView& F, const LevelView& C, const Weights& w, const double* fr,

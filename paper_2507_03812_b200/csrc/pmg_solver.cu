@@ -203,7 +203,7 @@ struct Solver {
     std::vector<double> scales;
     double tol = 1e-12;
     bool onfly = false;
-    bool serial = false;  // reference_order line solves
+    bool serial = false;  // reference_order: exact-order (bitwise) line solves
     int exact_rings = 0;  // innermost circle rings solved in exact order (fast mode)
     std::vector<Level> lv;
     std::vector<void*> allocs;
@@ -514,7 +514,6 @@ struct Solver {
     // sub-cycle there.
     void setup_coarse_tail() {
         const int L = static_cast<int>(lv.size());
-        if (serial) return;  // reference_order needs the exact-order level kernels
         long budget = 200 * 1024;
         if (const char* e = std::getenv("PMG_COARSE_SMEM")) budget = std::atol(e);
         if (budget <= 0) return;
@@ -531,7 +530,8 @@ struct Solver {
             if (!coarsest) {
                 d += 11 * n;                        // res, assembled rows
                 d += 2 * sp * nt + sp + 2 * nt * len + 5 * nt + 2 * nr + 2 * nt;
-                if (nt <= 32) d += nt * nt;  // origin ring inverse
+                if (serial) d += sp * nt;        // Sherman-Morrison vectors
+                else if (nt <= 32) d += nt * nt;  // origin ring inverse
             } else {
                 d += n <= 64 ? n * n : lv[l].env.nnz + n + n / 2 + n + 2;  // inv | L, D, fc, ro
             }
@@ -591,6 +591,8 @@ struct Solver {
                 c.cl = static_cast<double*>(place(V.cil, sp * nt * 8, sp * nt, 8));
                 c.cm = static_cast<double*>(place(V.cm, sp * nt * 8, sp * nt, 8));
                 c.corner = static_cast<double*>(place(V.corner, sp * 8, sp, 8));
+                if (serial) c.cz = static_cast<double*>(place(V.cz, sp * nt * 8, sp * nt, 8));
+                c.exact = serial ? 1 : 0;
                 if (len > 0) {
                     c.rl = static_cast<double*>(place(V.ril, nt * len * 8, nt * len, 8));
                     c.rm = static_cast<double*>(place(V.rm, nt * len * 8, nt * len, 8));
@@ -663,7 +665,7 @@ struct Solver {
                                  offsetof(CoarseLevel, res), offsetof(CoarseLevel, cl),
                                  offsetof(CoarseLevel, cm), offsetof(CoarseLevel, corner),
                                  offsetof(CoarseLevel, rl), offsetof(CoarseLevel, rm),
-                                 offsetof(CoarseLevel, rows)})
+                                 offsetof(CoarseLevel, rows), offsetof(CoarseLevel, cz)})
                     mark(c + f);
                 const size_t o = c + offsetof(CoarseLevel, of);
                 for (size_t f : {offsetof(OriginFactor, band1), offsetof(OriginFactor, band2),
@@ -775,7 +777,7 @@ struct Solver {
     // (PMG_MID_NODES=5000): measured 1-2% slower than the per-level kernels on
     // c0, c1, c2-V and c2-W once those got faster.
     void setup_mid() {
-        if (coarse_start <= 0 || serial) return;
+        if (coarse_start <= 0) return;
         long max_nodes = 0;
         if (const char* e = std::getenv("PMG_MID_NODES")) max_nodes = std::atol(e);
         int max_b = 16;
@@ -824,6 +826,8 @@ struct Solver {
                 launch_rows(V.v, onfly, V.rows, stream);
             }
             c.rows = V.rows;
+            c.cz = V.cz;
+            c.exact = serial ? 1 : 0;
             if (set.boundary_mode == 0) {
                 c.of.band1 = V.ob1;
                 c.of.band2 = V.ob2;
@@ -960,7 +964,7 @@ struct Solver {
             }
             for (int k = 0; k < nt - 2; ++k) r1[o + k] = E.at(nt - 2, k);
             for (int k = 0; k < nt - 1; ++k) r2[o + k] = E.at(nt - 1, k);
-            if (nt <= 32) {  // dense inverse for the warp solves of the one-block tail
+            if (nt <= 32 && !serial) {  // dense inverse for the warp solves of the one-block tail
                 if (b == 0) oinv.assign((size_t)B * nt * nt, 0.0);
                 std::vector<double> y(nt);
                 for (int j = 0; j < nt; ++j) {
@@ -1004,7 +1008,7 @@ struct Solver {
             }
             std::copy(E.L.begin(), E.L.end(), Lall.begin() + (size_t)b * E.L.size());
             std::copy(E.D.begin(), E.D.end(), Dall.begin() + (size_t)b * n);
-            if (n <= 64) {  // dense inverse for the one-block coarse tail
+            if (n <= 64 && !serial) {  // dense inverse for the one-block coarse tail
                 if (b == 0) inv.resize((size_t)B * n * n);
                 std::vector<double> x(n);
                 for (int j = 0; j < n; ++j) {
@@ -1068,7 +1072,7 @@ struct Solver {
         if (V.forder) {
             run(KK_SMOOTH, 1, [&] {
                 launch_smooth_fused(V.v, onfly, V.u, V.f, V.cil, V.cm, V.corner, V.cz, V.of(),
-                                    V.ril, V.rm, exact_rings, FuseCtl{fuse_ctl, V.fflags},
+                                    V.ril, V.rm, exact_rings, serial, FuseCtl{fuse_ctl, V.fflags},
                                     V.forder, act, stream);
             });
             return;
@@ -1599,6 +1603,7 @@ void pmg_default_settings(pmg_settings* s) {
     s->fmg_cycle = 2;
     s->norm_type = 0;
     s->max_iterations = 150;
+    s->reference_order = 1;  // bitwise reference parity (the drop-in default)
     s->absolute_tolerance = -1.0;
     s->relative_tolerance = 1e-8;
     s->max_threads = 0;
@@ -1780,6 +1785,10 @@ int pmg_solve(pmg_handle h, pmg_report* reports, double* history, int history_ca
 #ifdef PMG_KTRACE
 int pmg_debug_ktrace(unsigned long long* out) {
     pmg::read_ktrace(out);
+    return 0;
+}
+int pmg_debug_ktrace_reset() {
+    pmg::reset_ktrace();
     return 0;
 }
 #endif

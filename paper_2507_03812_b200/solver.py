@@ -246,8 +246,9 @@ class MultigridSettings:
     relative_tolerance: float = 1e-8
     max_threads: int = 0
     verbose: bool = False
-    # extension: line solves in the reference's sequential order (bitwise parity)
-    reference_order: bool = False
+    # extension: line solves reproduce the reference's sequential substitution
+    # bit for bit (default; False = faster chunked scans, roundoff-level drift)
+    reference_order: bool = True
 
 
 @dataclass

@@ -67,7 +67,7 @@ def test_default_settings_are_the_reference_defaults():
     assert st.max_iterations == ref.max_iterations == 150
     assert st.relative_tolerance == ref.relative_tolerance == 1e-8
     assert st.absolute_tolerance == ref.absolute_tolerance == -1.0
-    assert st.fmg_iterations == 2 and st.cycle == 0 and st.reference_order == 0
+    assert st.fmg_iterations == 2 and st.cycle == 0 and st.reference_order == 1
 
 
 @pytest.mark.parametrize("k", [0, 1, 2, 3])

@@ -1,14 +1,16 @@
 """End-to-end parity of the BASELINE configs at full size against the
-reference CPU solver (oracle/_ref) on identical seeded inputs.
+reference CPU solver (oracle/_ref) on identical seeded inputs -- the north
+star's contract: the same V-cycle iteration count and a final solution within
+1e-10 relative max-norm of the reference's.
 
-* reference_order=1: the GPU solve is BITWISE identical to the reference
-  (same iterates, same iteration count) -- the north star's "solution within
-  1e-10" with margin 0.
-* default (fast, parallel line scans): same iteration count, and the final u
-  within 1e-10 relative max-norm OR within the reference's own sensitivity to
-  a one-ulp change of f, measured in the test (the converged iterate of this
-  ill-conditioned system is only reproducible to ~kappa*eps: e.g. the reference
-  moves by 2.0e-9 on config 1 when half the entries of f move by one ulp).
+* default settings (reference_order=1, the mode bench.py measures): every line
+  solve reproduces the reference's sequential substitution bit for bit, so the
+  Take solves are BITWISE identical to the reference (same iterates, same
+  iteration count); Give (config 0) accumulates the smoother rhs by a gather
+  where the reference scatters in three phases, so it is held to 1e-10.
+* reference_order=0 (chunked parallel scans, opt-in, not benched): same
+  iteration count; the final u differs at the roundoff floor of this
+  ill-conditioned system (reported; not the parity contract).
 """
 import numpy as np
 import pytest
@@ -24,58 +26,77 @@ def relmax(a, b):
     return np.abs(a - b).max() / np.abs(b).max()
 
 
-def ulp_sensitivity(ref, f, out):
-    """relmax change of the reference's own solution when half the entries of
-    f move by one ulp (seeded)."""
-    rng = np.random.default_rng(0)
-    g = f.copy()
-    m = rng.random(f.size) < 0.5
-    g[m] = np.nextafter(g[m], np.inf)
-    return relmax(ref.solve(g)["u"], out["u"])
-
-
-def compare(k, cycle="V", reference_order=False, with_sensitivity=False):
+def compare(k, cycle="V", reference_order=True):
     ref = RefSolver(config_case(k, cycle=cycle))
     _, f = ref.seeded_rhs(SEED)
     out = ref.solve(f)
-    if with_sensitivity:
-        out["sensitivity"] = ulp_sensitivity(ref, f, out)
     geom, prob, grid, st, _ = pmg.baseline_config(k, cycle=cycle, reference_order=reference_order)
     gpu = pmg.MultigridSolver(geom, prob, grid, st)
     assert gpu.level_shape(0) == ref.levels[0] and gpu.num_levels() == ref.num_levels
     gpu.set_rhs(f)
     rep = gpu.solve()
     u = gpu.solution()
-    return out, rep, relmax(u, out["u"])
+    return out, rep, u
 
 
 @pytest.mark.parametrize("k,cycle", [(0, "V"), (1, "V"), (2, "V"), (2, "W")])
 def test_config_solve(k, cycle):
-    out, rep, err = compare(k, cycle, with_sensitivity=True)
-    sens = out["sensitivity"]
+    """The benched (default) mode: iteration count equal, relmax <= 1e-10;
+    Take configs bitwise, residual histories to 1e-8 relative (the GPU norm
+    is a parallel reduction)."""
+    out, rep, u = compare(k, cycle)
+    err = relmax(u, out["u"])
     print(f"config {k}{cycle}: ref {out['iterations']} its, gpu {rep.iterations} its, "
-          f"relmax {err:.3e}, reference 1-ulp sensitivity {sens:.3e}")
+          f"relmax {err:.3e}")
     assert rep.converged and out["converged"]
     assert rep.iterations == out["iterations"]
-    assert err < max(1e-10, sens)
-
-
-@pytest.mark.parametrize("k,cycle", [(1, "V"), (2, "V"), (2, "W")])
-def test_config_solve_bitwise(k, cycle):
-    """reference_order=1 (Take configs): the GPU solve reproduces the reference
-    bit for bit; residual norms (parallel reduction) to 1e-14 relative."""
-    out, rep, err = compare(k, cycle, reference_order=True)
-    assert rep.iterations == out["iterations"]
-    assert err == 0.0
+    assert err <= 1e-10
+    if k != 0:  # Take
+        assert np.array_equal(u, out["u"])
     assert np.allclose(np.array(rep.residual_norms), out["residual_norms"], rtol=1e-8, atol=0)
 
 
-def test_config3_sections():
-    """Config 3: batched GPU sections vs individual reference solves."""
-    idx = [0, 1, 2, 3]
+@pytest.mark.parametrize("k,cycle", [(1, "V"), (2, "W")])
+def test_config_solve_fast_mode(k, cycle):
+    """reference_order=0 (opt-in, not benched): same iteration count; the
+    solution differs from the reference at the roundoff floor (reported)."""
+    out, rep, u = compare(k, cycle, reference_order=False)
+    err = relmax(u, out["u"])
+    print(f"config {k}{cycle} fast line scans: relmax {err:.3e}")
+    assert rep.converged and rep.iterations == out["iterations"]
+    assert err < 1e-8
+
+
+def test_config3_all_sections():
+    """Config 3 in the benched mode: the 256-section batch (per-section alpha
+    scales, seeds SEED + i, per-section convergence masking) reproduces the 256
+    individual reference solves bit for bit."""
     scales = pmg.section_scales(256)
     assert np.array_equal(scales, ref_scales(256))
     geom, prob, grid, st, _ = pmg.baseline_config(3)
+    gpu = pmg.MultigridSolver(geom, prob, grid, st, n_sections=256, alpha_scales=scales)
+    gpu.seeded_rhs(SEED)  # section i: mt19937(SEED + i), f = A u* on the device
+    fs = gpu.get_rhs().reshape(256, -1)
+    gpu.solve()
+    u = gpu.solution().reshape(256, -1)
+    its = []
+    for i in range(256):
+        ref = RefSolver(config_case(3, alpha_scale=float(scales[i])))
+        _, f = ref.seeded_rhs(SEED + i)
+        assert np.array_equal(fs[i], f), f"section {i}: device-seeded rhs differs"
+        out = ref.solve(f)
+        rep = gpu.reports[i]
+        assert rep.converged and rep.iterations == out["iterations"], f"section {i}"
+        assert np.array_equal(u[i], out["u"]), f"section {i}: relmax {relmax(u[i], out['u']):.3e}"
+        its.append(rep.iterations)
+    print(f"256 sections bitwise; iterations {min(its)}..{max(its)}")
+
+
+def test_config3_sections_fast_mode():
+    """reference_order=0 on 4 sections: iteration counts equal (reported relmax)."""
+    idx = [0, 1, 2, 3]
+    scales = pmg.section_scales(256)
+    geom, prob, grid, st, _ = pmg.baseline_config(3, reference_order=False)
     gpu = pmg.MultigridSolver(geom, prob, grid, st, n_sections=len(idx),
                               alpha_scales=scales[idx])
     fs, outs = [], []
@@ -89,31 +110,6 @@ def test_config3_sections():
     u = gpu.solution().reshape(len(idx), -1)
     for j, (out, rep) in enumerate(zip(outs, gpu.reports)):
         err = relmax(u[j], out["u"])
-        print(f"section {idx[j]}: ref {out['iterations']} gpu {rep.iterations} relmax {err:.3e}")
+        print(f"section {idx[j]} fast: relmax {err:.3e}")
         assert rep.converged and rep.iterations == out["iterations"]
-        assert err < 1e-9  # below the reference's own 1-ulp sensitivity (8e-10 .. 2e-9)
-    # the device-seeded RHS equals the reference's f = A u* bitwise
-    gpu.seeded_rhs(SEED)
-    assert np.array_equal(gpu.get_rhs().reshape(len(idx), -1)[0], fs[0])
-
-
-def test_config3_sections_bitwise():
-    """reference_order=1: batched sections reproduce the per-section
-    reference solves bit for bit (per-section convergence masking included)."""
-    idx = [0, 1, 2, 3]
-    scales = pmg.section_scales(256)
-    geom, prob, grid, st, _ = pmg.baseline_config(3, reference_order=True)
-    gpu = pmg.MultigridSolver(geom, prob, grid, st, n_sections=len(idx),
-                              alpha_scales=scales[idx])
-    fs, outs = [], []
-    for i in idx:
-        ref = RefSolver(config_case(3, alpha_scale=float(scales[i])))
-        _, f = ref.seeded_rhs(SEED + i)
-        fs.append(f)
-        outs.append(ref.solve(f))
-    gpu.set_rhs(np.concatenate(fs))
-    gpu.solve()
-    u = gpu.solution().reshape(len(idx), -1)
-    for j, (out, rep) in enumerate(zip(outs, gpu.reports)):
-        assert rep.iterations == out["iterations"]
-        assert np.array_equal(u[j], out["u"])
+        assert err < 1e-8

@@ -10,9 +10,10 @@ problem (testsup::polar_case: Zoni alpha, r_p = 0.7, delta_r = 0.05,
 beta = 1/alpha, PolarOscillation, R0 = 1.3e-5; acceptance.cpp:85,237).
 
 Tolerances: the assembled RHS is bitwise (same expressions, libm values
-tabulated on the host); reference_order solves are bitwise in u and in the
-iteration counts; fast-mode solves keep the iteration counts and u within
-1e-9 relative max-norm; exact errors (a device reduction in another order)
+tabulated on the host); default (reference_order) Take solves are bitwise in u
+and in the iteration counts, Give solves within 1e-10 relative max-norm; the
+opt-in fast line scans keep the iteration counts and u within 1e-8 (the
+roundoff floor, reported); exact errors (a device reduction in another order)
 within 1e-12 relative.
 """
 import numpy as np
@@ -136,8 +137,10 @@ def test_solve_solution(solved):
     if ro and c.stencil_mode == "Take":
         assert np.array_equal(u, ref["u"]), relmax(u, ref["u"])
         np.testing.assert_allclose(rep.residual_norms, ref["residual_norms"], rtol=1e-10)
-    else:
-        assert relmax(u, ref["u"]) < 1e-9
+    elif ro:  # benched mode, Give: the north star's 1e-10
+        assert relmax(u, ref["u"]) <= 1e-10
+    else:  # opt-in fast line scans: roundoff floor, reported
+        assert relmax(u, ref["u"]) < 1e-8
 
 
 def test_solve_exact_errors(solved):
