@@ -1075,260 +1075,6 @@ __device__ void origin_solve_seq(double* Y, double* B1, double* B2, double* X,
     __syncthreads();
 }
 
-// Across-origin ring in the reference's exact order (line_algebra.cpp:211-255,
-// permutation smoother.cpp:42-46), all threads of the block: the band
-// substitutions are 2nd-order recurrences, solved like line_solve_ex -- the
-// 2x2-map scan of origin_solve gives approximate states at the chunk
-// boundaries, every thread restarts the exact recurrence one chunk early and
-// waves recompute the chunks whose entry state differs from their
-// predecessor's result bit for bit.  The two dense closing rows are
-// sequential sums in the reference's k order (two independent chains on one
-// thread); the diagonal scaling and the dense rows' column updates are per
-// element.  Y: rhs in NATURAL order (padded) in, solution out; X, B1, B2:
-// padded workspaces (the band factors are staged in B1, B2); scr: >= 64 +
-// 4 * blockDim.x doubles.
-template <int K>
-__device__ void origin_solve_ex(double* Y, double* X, double* B1, double* B2,
-                                const OriginFactor& of, int b, int n, double* scr) {
-    static_assert(K >= 2, "a chunk must hold the two rows of the recurrence state");
-    const long o = (long)b * n;
-    const double* __restrict__ gb1 = of.band1 + o;
-    const double* __restrict__ gb2 = of.band2 + o;
-    const double* __restrict__ r1 = of.row1 + o;
-    const double* __restrict__ r2 = of.row2 + o;
-    const double* __restrict__ D = of.D + o;
-    const int h = n / 2, nb = n - 2, T = blockDim.x, t = threadIdx.x;
-    const int j0 = t * K;
-    const bool live = j0 < nb;
-    double* Sa = scr + 64;   // approximate entry states (2 per thread)
-    double* Se = Sa + 2 * T;  // chunk results next to the neighbour (2 per thread, 2 buffers)
-    for (int k = t; k < n; k += T) {
-        X[P(k)] = Y[P(operm(k, h))];
-        B1[P(k)] = k < nb ? gb1[k] : 0.0;
-        B2[P(k)] = k < nb ? gb2[k] : 0.0;
-    }
-    __syncthreads();
-    KT(6);
-    double z[K];
-    int waves = 0;
-    // ---- forward band: z_i = (x_i - L(i,i-2) z_{i-2}) - L(i,i-1) z_{i-1}
-    // branch-free (selects): loads hoist ahead of the chain
-    auto fstep = [&](int i, double& zm2, double& zm1) {
-        const double x = X[P(i)], l2 = B2[P(i)], l1 = B1[P(i)];
-        const double s2 = x - l2 * zm2;
-        const double sa = i >= 2 ? s2 : x;
-        const double s1 = sa - l1 * zm1;
-        const double sum = i >= 1 ? s1 : sa;
-        zm2 = zm1;
-        zm1 = sum;
-    };
-    {
-        Map2 m = {1.0, 0.0, 0.0, 1.0, 0.0, 0.0};
-#pragma unroll
-        for (int q = 0; q < K; ++q) {
-            const int i = j0 + q;
-            if (i < nb) {
-                const double l1 = i >= 1 ? B1[P(i)] : 0.0, l2 = i >= 2 ? B2[P(i)] : 0.0;
-                const Map2 mi = {0.0, 1.0, -l2, -l1, 0.0, X[P(i)]};
-                m = compose2(mi, m);
-            }
-        }
-        double a0, a1;
-        block_scan2<true>(m, a0, a1, scr);
-        Sa[2 * t] = a0;
-        Sa[2 * t + 1] = a1;
-        __syncthreads();
-        KT(7);
-        double s0 = 0.0, s1 = 0.0;  // this trajectory's (z_{j0-2}, z_{j0-1})
-        if (live && t >= 1) {
-            double zm2 = t >= 2 ? Sa[2 * (t - 1)] : 0.0, zm1 = t >= 2 ? Sa[2 * (t - 1) + 1] : 0.0;
-#pragma unroll
-            for (int q = 0; q < K; ++q) fstep(j0 - K + q, zm2, zm1);
-            s0 = zm2;
-            s1 = zm1;
-        }
-        auto chunk = [&](double zm2, double zm1) {
-#pragma unroll
-            for (int q = 0; q < K; ++q) {  // rows past nb: computed on row nb-1, not stored
-                double a = zm2, c = zm1;
-                fstep(min(j0 + q, nb - 1), a, c);
-                if (j0 + q < nb) {
-                    zm2 = a;
-                    zm1 = c;
-                }
-                z[q] = zm1;
-            }
-        };
-        auto publish = [&](int buf) {  // the chunk's last two rows (the successor's entry state)
-            Se[buf * 2 * T + 2 * t] = z[K - 2];
-            Se[buf * 2 * T + 2 * t + 1] = z[K - 1];
-        };
-        if (live) chunk(s0, s1);
-        publish(0);
-        __syncthreads();
-        for (int cur = 0;; cur ^= 1) {
-            const double* Sc = Se + cur * 2 * T;
-            const double p0 = t >= 1 ? Sc[2 * (t - 1)] : 0.0, p1 = t >= 1 ? Sc[2 * (t - 1) + 1] : 0.0;
-            const bool bad = live && t >= 1 && !(same_bits(s0, p0) && same_bits(s1, p1));
-            if (bad) {
-                s0 = p0;
-                s1 = p1;
-                chunk(s0, s1);
-            }
-            publish(cur ^ 1);
-            if (!__syncthreads_or(bad)) break;
-            ++waves;
-        }
-    }
-    KT(8);
-    KTV(28, waves);
-    waves = 0;
-#pragma unroll
-    for (int q = 0; q < K; ++q)
-        if (j0 + q < nb) X[P(j0 + q)] = z[q];
-    __syncthreads();
-    // ---- dense closing rows: sequential sums in the reference's k order;
-    // the products RN(L(i,k) z_k) are formed in parallel (into Y and W, both
-    // free here), one thread runs the two chains of subtractions
-    double* W = B2;  // reloaded before the backward band
-    for (int k = t; k < nb; k += T) {
-        const double zk = X[P(k)];
-        Y[P(k)] = r1[k] * zk;
-        W[P(k)] = r2[k] * zk;
-    }
-    __syncthreads();
-    if (t == 0) {
-        // subtracting +0 is an identity, so rows outside [fc, nb) subtract 0
-        double s1 = X[P(n - 2)], s2 = X[P(n - 1)];
-        const int f1 = of.fc1, f2 = of.fc2;
-        for (int k0 = min(f1, f2); k0 < nb; k0 += 8) {
-            double p1[8], p2[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const int k = k0 + q;
-                p1[q] = (k < nb && k >= f1) ? Y[P(k)] : 0.0;
-                p2[q] = (k < nb && k >= f2) ? W[P(k)] : 0.0;
-            }
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                s1 -= p1[q];
-                s2 -= p2[q];
-            }
-        }
-        if (n - 2 >= f2) s2 -= r2[n - 2] * s1;
-        X[P(n - 2)] = s1;
-        X[P(n - 1)] = s2;
-    }
-    __syncthreads();
-    KT(9);
-    // ---- diagonal, then the dense rows' column updates (row n-1 first)
-    for (int k = t; k < n; k += T) {
-        X[P(k)] /= D[k];
-        B2[P(k)] = k < nb ? gb2[k] : 0.0;
-    }
-    __syncthreads();
-    if (t == 0 && n - 2 >= of.fc2) X[P(n - 2)] -= r2[n - 2] * X[P(n - 1)];
-    __syncthreads();
-    {
-        const double xn1 = X[P(n - 1)], xn2 = X[P(n - 2)];
-        for (int k = t; k < nb; k += T) {
-            double x = X[P(k)];
-            if (k >= of.fc2) x -= r2[k] * xn1;
-            if (k >= of.fc1) x -= r1[k] * xn2;
-            X[P(k)] = x;
-        }
-    }
-    __syncthreads();
-    KT(10);
-    // ---- backward band: x_k = (g_k - L(k+2,k) x_{k+2}) - L(k+1,k) x_{k+1}
-    auto bstep = [&](int k, double& xp1, double& xp2) {
-        const double g = X[P(k)];
-        const double l2 = B2[P(k + 2 < nb ? k + 2 : 0)], l1 = B1[P(k + 1 < nb ? k + 1 : 0)];
-        const double s2 = g - l2 * xp2;
-        const double sa = k + 2 < nb ? s2 : g;
-        const double s1 = sa - l1 * xp1;
-        const double x = k + 1 < nb ? s1 : sa;
-        xp2 = xp1;
-        xp1 = x;
-    };
-    {
-        Map2 g = {1.0, 0.0, 0.0, 1.0, 0.0, 0.0};
-#pragma unroll
-        for (int q = K - 1; q >= 0; --q) {
-            const int k = j0 + q;
-            if (k < nb) {
-                const double l1 = k + 1 < nb ? B1[P(k + 1)] : 0.0;
-                const double l2 = k + 2 < nb ? B2[P(k + 2)] : 0.0;
-                const Map2 mk = {-l1, -l2, 1.0, 0.0, X[P(k)], 0.0};
-                g = compose2(mk, g);
-            }
-        }
-        double a0, a1;
-        block_scan2<false>(g, a0, a1, scr);  // entry state (x_{j0+K}, x_{j0+K+1})
-        Sa[2 * t] = a0;
-        Sa[2 * t + 1] = a1;
-        __syncthreads();
-        const bool succ = j0 + K < nb;
-        double s0 = 0.0, s1 = 0.0;  // this trajectory's (x_{j0+K}, x_{j0+K+1})
-        if (live && succ) {
-            double xp1 = j0 + 2 * K < nb ? Sa[2 * (t + 1)] : 0.0;
-            double xp2 = j0 + 2 * K < nb ? Sa[2 * (t + 1) + 1] : 0.0;
-#pragma unroll
-            for (int q = K - 1; q >= 0; --q) {
-                double a = xp1, c = xp2;
-                bstep(min(j0 + K + q, nb - 1), a, c);
-                if (j0 + K + q < nb) {
-                    xp1 = a;
-                    xp2 = c;
-                }
-            }
-            s0 = xp1;
-            s1 = xp2;
-        }
-        auto chunk = [&](double xp1, double xp2) {
-#pragma unroll
-            for (int q = K - 1; q >= 0; --q) {
-                double a = xp1, c = xp2;
-                bstep(min(j0 + q, nb - 1), a, c);
-                if (j0 + q < nb) {
-                    xp1 = a;
-                    xp2 = c;
-                }
-                z[q] = xp1;
-            }
-        };
-        auto publish = [&](int buf) {  // the chunk's first two rows (the predecessor's entry state)
-            Se[buf * 2 * T + 2 * t] = z[0];
-            Se[buf * 2 * T + 2 * t + 1] = z[1];
-        };
-        if (live) chunk(s0, s1);
-        publish(0);
-        __syncthreads();
-        for (int cur = 0;; cur ^= 1) {
-            const double* Sc = Se + cur * 2 * T;
-            const double p0 = t + 1 < T ? Sc[2 * (t + 1)] : 0.0;
-            const double p1 = t + 1 < T ? Sc[2 * (t + 1) + 1] : 0.0;
-            const bool bad = live && succ && !(same_bits(s0, p0) && same_bits(s1, p1));
-            if (bad) {
-                s0 = p0;
-                s1 = p1;
-                chunk(s0, s1);
-            }
-            publish(cur ^ 1);
-            if (!__syncthreads_or(bad)) break;
-            ++waves;
-        }
-    }
-    KT(11);
-    KTV(29, waves);
-#pragma unroll
-    for (int q = 0; q < K; ++q)
-        if (j0 + q < nb) X[P(j0 + q)] = z[q];
-    __syncthreads();
-    for (int k = t; k < n; k += T) Y[P(operm(k, h))] = X[P(k)];
-    __syncthreads();
-}
-
 // Serial envelope solve of the across-origin ring (reference
 // line_algebra.cpp:211-255 with permutation smoother.cpp:42-46); run by one
 // thread on the shared-memory rhs.
