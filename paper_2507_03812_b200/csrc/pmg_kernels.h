@@ -7,6 +7,9 @@
 
 namespace pmg {
 
+// first kernel-launch error since the last call, else cudaGetLastError()
+cudaError_t last_error();
+
 // Envelope LDL^T of the across-origin ring in antipodally interleaved order
 // (reference smoother.cpp:33-49, line_algebra.cpp:122-255).  Rows < n-2
 // have bandwidth <= 2; the two closing rows are dense (Moebius ladder).

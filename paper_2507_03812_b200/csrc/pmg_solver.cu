@@ -910,7 +910,7 @@ struct Solver {
         int hb = 0;
         PMG_CUDA(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, stream));
         PMG_CUDA(cudaStreamSynchronize(stream));
-        PMG_CUDA(cudaGetLastError());
+        PMG_CUDA(last_error());
         if (hb) throw PmgError(PMG_ERUNTIME, msg);
     }
 
@@ -1303,7 +1303,7 @@ struct Solver {
         int hb = 0;
         PMG_CUDA(cudaMemcpyAsync(&hb, d_bad, sizeof(int), cudaMemcpyDeviceToHost, stream));
         PMG_CUDA(cudaStreamSynchronize(stream));
-        PMG_CUDA(cudaGetLastError());
+        PMG_CUDA(last_error());
         if (hb == 1) throw PmgError(PMG_ERUNTIME, "singular Jacobian: mapping degenerate at queried point");
         if (hb == 2)
             throw PmgError(PMG_ERUNTIME,
@@ -1406,7 +1406,7 @@ struct Solver {
         PMG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
-        PMG_CUDA(cudaGetLastError());
+        PMG_CUDA(last_error());
         last_solve_ms = ms;
         collect_profile();
         if (coarse_params.trace && mid_start < 0) print_tail_trace();
@@ -1490,7 +1490,7 @@ struct Solver {
     }
     void sync_check() {
         PMG_CUDA(cudaStreamSynchronize(stream));
-        PMG_CUDA(cudaGetLastError());
+        PMG_CUDA(last_error());
     }
     void ensure_flush() {
         if (!flush_buf) {
@@ -2017,7 +2017,7 @@ int pmg_time_kernel(pmg_handle h, int kind, int level, int reps, int flush_l2,
         }
         cudaEventDestroy(a);
         cudaEventDestroy(b);
-        PMG_CUDA(cudaGetLastError());
+        PMG_CUDA(pmg::last_error());
         *ms_per_call = total / reps;
     });
 }
