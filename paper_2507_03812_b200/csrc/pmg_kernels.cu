@@ -21,6 +21,7 @@
 #include <utility>
 
 #include "pmg_kernels.h"
+#include "pmg_lines.cuh"
 
 namespace pmg {
 
@@ -63,18 +64,8 @@ __device__ unsigned long long g_ktrace[32];
     } while (0)
 #endif
 
-// Programmatic dependent launch: every kernel of the solve lets the next one
-// in the stream start launching at once and waits for its predecessor's
-// results before touching them (griddepcontrol; no-ops without the launch
-// attribute).
-__device__ __forceinline__ void pdl_enter() {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-}
-
 namespace {
 
-constexpr unsigned FULL = 0xffffffffu;
 // The across-origin ring is solved in the reference's exact substitution
 // order (origin_solve_exact) in reference_order mode and for rings of at most
 // this length; longer rings use the parallel 2x2-map scan (origin_solve).
@@ -539,16 +530,6 @@ __device__ void origin_solve(double* Y, double* X, const OriginFactor& of, int b
     KT(15);
 }
 
-// Correctly rounded a / l given r = RN(1/l) (Markstein): q0 = RN(a r) is
-// within 1 ulp, e = a - l q0 is exact (FMA), RN(q0 + e r) = RN(a / l).  The
-// reciprocal is off the dependency chain, so a sequential substitution costs
-// 3 dependent FP64 ops per division instead of a full IEEE division.
-__device__ __forceinline__ double xdiv(double a, double l, double r) {
-    const double q0 = a * r;
-    const double e = fma(-l, q0, a);
-    return fma(e, r, q0);
-}
-
 // Sequential L L^T solve in the reference's exact operation order
 // (tridiag_solve, line_algebra.cpp:42-62) -- bitwise identical results.
 // Run by ONE thread on shared memory; Ld holds the raw L diagonal.
@@ -596,9 +577,6 @@ __device__ void tri_solve_exact(double* Y, const double* Ld, const double* M, in
 // (padded shared-memory rows); z: the Sherman-Morrison vector z = T^{-1}(e_1
 // + e_n), computed at setup by the same exact sequence (k_circle_z).
 // scr: >= 64 + 3*blockDim.x doubles (line_smem(n, true) reserves 64 + 6*512).
-__device__ __forceinline__ bool same_bits(double a, double b) {
-    return __double_as_longlong(a) == __double_as_longlong(b);
-}
 // forward row j of L y = b (tridiag_solve's first loop), v = y_{j-1}.
 // Branch-free (selects, clamped indices): the rows of a chunk unroll into
 // straight-line code whose shared-memory loads the scheduler hoists ahead of
@@ -3127,29 +3105,6 @@ __global__ void k_coarse(EnvFactor E, const double* __restrict__ f, double* __re
 // parameter so the kernel carries only the code of its own line length (the
 // one-block tail is instruction-fetch bound when the code is large).
 
-template <int NV, bool FWD>
-__device__ __forceinline__ void warp_scan(double A, double (&B)[NV], double (&yin)[NV]) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const double Ao = FWD ? __shfl_up_sync(FULL, A, d) : __shfl_down_sync(FULL, A, d);
-        double Bo[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v)
-            Bo[v] = FWD ? __shfl_up_sync(FULL, B[v], d) : __shfl_down_sync(FULL, B[v], d);
-        if (FWD ? (lane >= d) : (lane + d < 32)) {
-#pragma unroll
-            for (int v = 0; v < NV; ++v) B[v] = A * Bo[v] + B[v];
-            A = A * Ao;
-        }
-    }
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-        const double prev = FWD ? __shfl_up_sync(FULL, B[v], 1) : __shfl_down_sync(FULL, B[v], 1);
-        yin[v] = lane == (FWD ? 0 : 31) ? 0.0 : prev;
-    }
-}
-
 __device__ __forceinline__ void warp_scan2(Map2 a, bool fwd, double& in0, double& in1) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -3393,299 +3348,6 @@ __device__ __forceinline__ void warp_line_solve_ex(double (&y)[KW], const double
         for (int q = 0; q < KW; ++q)
             if (row_in(q, j0 + q)) y[q] -= tau * z[j0 + q];
     }
-}
-
-// ---------------------------------------------- warp-per-line radial sweep
-// Many radial lines of at most 32*KW nodes (config 3: 65536 spokes of 431
-// nodes per colour): one WARP per spoke and no block barriers.  The warp
-// gathers the rhs of rows lane, lane+32, ... (coalesced loads of the
-// spoke-major arrays; all operands of a row issued before its arithmetic,
-// the same expressions as radial_body, so the rhs is bitwise the same) and
-// stages it with the line's factors in its own shared-memory slice.  Each
-// lane then takes KE consecutive rows -- KE odd, so the 8-byte shared-memory
-// reads of a half-warp hit 16 distinct banks pairs -- and the warp solves the
-// line by warp scans: in the reference's exact order by speculation and
-// verification waves (warp_tri_ex) or, fast mode, with the scans' values
-// (warp_tri_fast).  The result goes back through the slice, coalesced.
-struct RadLine {  // per-spoke constants of the lean interior rows
-    int dTM, dTP;
-    double km, kp, rkm, rkp;
-};
-
-// rhs row i of radial line t (reference smoother.cpp:184-205): the branches
-// of radial_body for one row.
-template <bool ONFLY>
-__device__ __forceinline__ double radial_rhs(const LevelView& L, const CoefAt<ONFLY>& cf,
-                                             const double* __restrict__ U,
-                                             const double* __restrict__ F, long off, int t,
-                                             int base, const RadLine& R, int i) {
-    const int s = L.split + i, p = base + i;
-    if (L.rows) {
-        const double* Rw = L.rows + (off / L.n) * 10 * L.n;
-        const int n = L.n;
-        const Nbr q = neighbours(L, s, t, p);
-        double acc = F[p];
-        if (s == L.split) acc -= Rw[1 * n + p] * U[q.pSM];
-        acc -= Rw[3 * n + p] * U[q.pTM];
-        acc -= Rw[4 * n + p] * U[q.pTP];
-        acc -= Rw[5 * n + p] * U[q.pSMTM];
-        acc -= Rw[6 * n + p] * U[q.pSMTP];
-        acc -= Rw[7 * n + p] * U[q.pSPTM];
-        acc -= Rw[8 * n + p] * U[q.pSPTP];
-        return acc;
-    }
-    if (!ONFLY && i >= 1 && i <= L.len - 2) {
-        const double* __restrict__ ATT = L.att + off;
-        const double* __restrict__ ART = L.art + off;
-        const int dTM = R.dTM, dTP = R.dTP;
-        const double fP = F[p];
-        const double attP = ATT[p], attM = ATT[p + dTM], attQ = ATT[p + dTP];
-        const double artM = ART[p + dTM], artQ = ART[p + dTP];
-        const double artSM = ART[p - 1], artSP = ART[p + 1];
-        const double uM = U[p + dTM], uQ = U[p + dTP];
-        const double uMM = U[p + dTM - 1], uQM = U[p + dTP - 1];
-        const double uMP = U[p + dTM + 1], uQP = U[p + dTP + 1];
-        const double hbar = 0.5 * (L.h[s - 1] + L.h[s]);
-        const double south = -xdiv(hbar, R.km, R.rkm) * (attP + attM);
-        const double north = -xdiv(hbar, R.kp, R.rkp) * (attP + attQ);
-        double acc = fP;
-        acc -= south * uM;
-        acc -= north * uQ;
-        acc -= (-(artM + artSM) * 0.25) * uMM;
-        acc -= ((artSM + artQ) * 0.25) * uQM;
-        if (s + 1 < L.nr - 1 || !L.dir(s + 1)) {
-            acc -= ((artM + artSP) * 0.25) * uMP;
-            acc -= (-(artSP + artQ) * 0.25) * uQP;
-        }
-        return acc;
-    }
-    if (L.dir(s)) return F[p];
-    const Nbr q = neighbours(L, s, t, p);
-    const Row Rr = make_row_fast(L, cf, s, t, p, q);
-    double acc = F[p];
-    if (s == L.split && Rr.has_sm) acc -= Rr.sm * U[q.pSM];
-    acc -= Rr.tm * U[q.pTM];
-    acc -= Rr.tp * U[q.pTP];
-    if (Rr.has_sm) {
-        acc -= Rr.mm * U[q.pSMTM];
-        acc -= Rr.mp * U[q.pSMTP];
-    }
-    if (Rr.has_sp) {
-        acc -= Rr.pm * U[q.pSPTM];
-        acc -= Rr.pp * U[q.pSPTP];
-    }
-    return acc;
-}
-
-// L L^T x = b of one line by one warp (tridiag_solve, line_algebra.cpp:42-62).
-// y[q]: row j0 + q (j0 = lane * KE, q < KE) of b on entry, of x on exit;
-// Ld / M: raw L diagonal and sub-diagonal of the line (shared memory).
-// EXACT: the reference's sequential substitution bit for bit -- the warp
-// scan's approximate chunk-entry values seed a restart of the recurrence one
-// chunk early (the recurrences contract, |m/l| < 1, so the restarted
-// trajectory merges with the reference's bit for bit within a few rows);
-// lanes whose trajectory at their predecessor's last row differs from the
-// predecessor's result recompute from that result, in waves (ballots), until
-// every lane starts from its predecessor's end bit for bit -- which is then
-// the sequential substitution by induction from row 0.  Fast: the scan's
-// values (reciprocal multiplies; differs in the last bits).
-template <int KW, bool EXACT>
-__device__ __forceinline__ void warp_tri(double (&y)[KW], const double* __restrict__ Ld,
-                                         const double* __restrict__ M, int n, int KE) {
-    const int lane = threadIdx.x & 31, j0 = lane * KE;
-    const bool live = j0 < n;
-    double b[KW], rc[KW];
-#pragma unroll
-    for (int q = 0; q < KW; ++q) {
-        const int j = j0 + q;
-        const bool in = q < KE && j < n;
-        b[q] = y[q];
-        rc[q] = in ? __drcp_rn(Ld[j]) : 0.0;
-    }
-    // ---- forward: y_j = (b_j - m_{j-1} y_{j-1}) / l_j
-    double A = 1.0, Bv[1] = {0.0};
-#pragma unroll
-    for (int q = 0; q < KW; ++q) {
-        const int j = j0 + q;
-        if (q < KE && j < n) {
-            const double a = j > 0 ? -(M[j - 1] * rc[q]) : 0.0;
-            Bv[0] = a * Bv[0] + b[q] * rc[q];
-            A = a * A;
-        }
-    }
-    double yin[1];
-    warp_scan<1, true>(A, Bv, yin);
-    if (!EXACT) {
-        double v = yin[0];
-#pragma unroll
-        for (int q = 0; q < KW; ++q) {
-            const int j = j0 + q;
-            if (q < KE && j < n) {
-                v = (b[q] - (j > 0 ? M[j - 1] : 0.0) * v) * rc[q];
-                y[q] = v;
-            }
-        }
-    } else {
-        auto fstep = [&](double bj, int j, double v, double r) {
-            return xdiv(j == 0 ? bj : bj - M[j > 0 ? j - 1 : 0] * v, Ld[j], r);
-        };
-        double st;
-        {
-            double v = __shfl_up_sync(FULL, yin[0], 1);  // approx. value entering lane-1's rows
-#pragma unroll
-            for (int q = 0; q < KW; ++q) {
-                const double bp = __shfl_up_sync(FULL, b[q], 1);
-                const double rp = __shfl_up_sync(FULL, rc[q], 1);
-                if (lane >= 1 && live && q < KE) v = fstep(bp, j0 - KE + q, v, rp);
-            }
-            st = v;
-        }
-        auto fchunk = [&](double v) {
-#pragma unroll
-            for (int q = 0; q < KW; ++q) {
-                const int j = j0 + q;
-                if (q < KE && j < n) {
-                    v = fstep(b[q], j, v, rc[q]);
-                    y[q] = v;
-                }
-            }
-            return v;
-        };
-        double e = live ? fchunk(st) : 0.0;
-        for (;;) {
-            const double pe = __shfl_up_sync(FULL, e, 1);
-            const bool bad = lane >= 1 && live && !same_bits(st, pe);
-            if (!__any_sync(FULL, bad)) break;
-            if (bad) {
-                st = pe;
-                e = fchunk(st);
-            }
-        }
-    }
-    // ---- backward: x_j = (y_j - m_j x_{j+1}) / l_j
-#pragma unroll
-    for (int q = 0; q < KW; ++q) b[q] = y[q];
-    double G = 1.0, Dv[1] = {0.0};
-#pragma unroll
-    for (int q = KW - 1; q >= 0; --q) {
-        const int j = j0 + q;
-        if (q < KE && j < n) {
-            const double g = j < n - 1 ? -(M[j] * rc[q]) : 0.0;
-            Dv[0] = g * Dv[0] + b[q] * rc[q];
-            G = g * G;
-        }
-    }
-    double xin[1];
-    warp_scan<1, false>(G, Dv, xin);
-    if (!EXACT) {
-        double v = xin[0];
-#pragma unroll
-        for (int q = KW - 1; q >= 0; --q) {
-            const int j = j0 + q;
-            if (q < KE && j < n) {
-                v = (b[q] - (j < n - 1 ? M[j] : 0.0) * v) * rc[q];
-                y[q] = v;
-            }
-        }
-        return;
-    }
-    auto bstep = [&](double yj, int j, double v, double r) {
-        return xdiv(j == n - 1 ? yj : yj - M[j] * v, Ld[j], r);
-    };
-    const bool succ = j0 + KE < n;
-    double st;
-    {
-        // approximate value entering lane+1's rows from above; exact when
-        // lane+1 holds row n-1
-        double v = __shfl_down_sync(FULL, xin[0], 1);
-#pragma unroll
-        for (int q = KW - 1; q >= 0; --q) {
-            const double yn = __shfl_down_sync(FULL, b[q], 1);
-            const double rn = __shfl_down_sync(FULL, rc[q], 1);
-            const int j = j0 + KE + q;
-            if (succ && q < KE && j < n) v = bstep(yn, j, v, rn);
-        }
-        st = v;
-    }
-    auto bchunk = [&](double v) {
-#pragma unroll
-        for (int q = KW - 1; q >= 0; --q) {
-            const int j = j0 + q;
-            if (q < KE && j < n) {
-                v = bstep(b[q], j, v, rc[q]);
-                y[q] = v;
-            }
-        }
-        return v;
-    };
-    double e = live ? bchunk(st) : 0.0;
-    for (;;) {
-        const double pe = __shfl_down_sync(FULL, e, 1);
-        const bool bad = live && succ && !same_bits(st, pe);
-        if (!__any_sync(FULL, bad)) break;
-        if (bad) {
-            st = pe;
-            e = bchunk(st);
-        }
-    }
-}
-
-// odd rows per lane >= ceil(n / 32) (conflict-free chunked shared-memory reads)
-__host__ __device__ __forceinline__ int warp_ke(int n) { return ((n + 31) >> 5) | 1; }
-
-template <bool ONFLY, int KW, bool EXACT>
-__global__ void __launch_bounds__(128) k_radial_warp(LevelView L, double* __restrict__ u,
-                                                     const double* __restrict__ f,
-                                                     const double* __restrict__ ril,
-                                                     const double* __restrict__ rm, int parity,
-                                                     const int* __restrict__ active) {
-    pdl_enter();
-    extern __shared__ double smem[];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int lines = (L.nt - parity + 1) >> 1;
-    const long g = (long)blockIdx.x * (blockDim.x >> 5) + w;
-    if (g >= (long)lines * L.B) return;  // whole warps only
-    const int b = (int)(g / lines);
-    const int t = parity + 2 * (int)(g - (long)b * lines);
-    if (active && !active[b]) return;
-    const int len = L.len, KE = warp_ke(len), stride = 32 * KE;
-    const long off = (long)b * L.n;
-    double* U = u + off;
-    const double* F = f + off;
-    const int base = L.split * L.nt + t * len;
-    const long fo = ((long)b * L.nt + t) * len;
-    double* Y = smem + (long)w * 3 * stride;
-    double* Ld = Y + stride;
-    double* Ms = Ld + stride;
-    RadLine R;
-    {
-        const int tm = L.tminus(t), tp = L.tplus(t);
-        R.dTM = (tm - t) * len;
-        R.dTP = (tp - t) * len;
-        R.km = L.k[tm];
-        R.kp = L.k[t];
-        R.rkm = L.rk[tm];
-        R.rkp = L.rk[t];
-    }
-    const CoefAt<ONFLY> cf{&L, off, b};
-#pragma unroll 2
-    for (int i = lane; i < len; i += 32) {
-        Ld[i] = ril[fo + i];
-        Ms[i] = rm[fo + i];
-        Y[i] = radial_rhs<ONFLY>(L, cf, U, F, off, t, base, R, i);
-    }
-    __syncwarp();
-    const int j0 = lane * KE;
-    double y[KW];
-#pragma unroll
-    for (int q = 0; q < KW; ++q) y[q] = (q < KE && j0 + q < len) ? Y[j0 + q] : 0.0;
-    warp_tri<KW, EXACT>(y, Ld, Ms, len, KE);
-    __syncwarp();
-#pragma unroll
-    for (int q = 0; q < KW; ++q)
-        if (q < KE && j0 + q < len) Y[j0 + q] = y[q];
-    __syncwarp();
-    for (int i = lane; i < len; i += 32) U[base + i] = Y[i];
 }
 
 // Across-origin ring of a tail level in the reference's exact order
@@ -4409,6 +4071,12 @@ __global__ void k_set_active(int* active, int* count, int* conv, int* remaining,
     if (b == 0) *remaining = B;
 }
 
+// Loop condition of the solve's WHILE graph node (multigrid.cpp:328-340):
+// another cycle runs while any section is still iterating.
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const int* __restrict__ remaining) {
+    if (threadIdx.x == 0) cudaGraphSetConditional(h, *remaining != 0 ? 1u : 0u);
+}
+
 __global__ void k_flush(double* p, long n) {
     for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long)gridDim.x * blockDim.x)
@@ -4416,26 +4084,6 @@ __global__ void k_flush(double* p, long n) {
 }
 
 // ------------------------------------------------------------ launch helpers
-// Opt a kernel into the full 227 KB of dynamic shared memory once per
-// (kernel, device); launches then pass their exact size.
-template <class KernelT>
-void set_smem(KernelT kern, size_t bytes) {
-    (void)bytes;
-    static std::mutex mu;
-    static std::set<std::pair<const void*, int>> done;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const auto key = std::make_pair(reinterpret_cast<const void*>(kern), dev);
-    std::lock_guard<std::mutex> lock(mu);
-    if (done.count(key)) return;
-    cudaFuncAttributes fa;
-    int optin = 227 * 1024;
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess) optin -= (int)fa.sharedSizeBytes;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-    done.insert(key);
-}
-
 // chunk size K and threads T for a line of n rows: T = 32*ceil(ceil(n/K)/32) <= 512
 // Threads per line: wide CTAs (short per-thread chunks) when few lines run
 // concurrently (latency), narrow CTAs when the batch of lines fills the GPU
@@ -4479,7 +4127,7 @@ inline int exact_mode(int n) { return line_smem(n, true) <= 227 * 1024 ? 1 : 2; 
 // First failed launch since the last check (a failed cudaLaunchKernelEx would
 // otherwise only surface through cudaGetLastError, which other probes clear).
 static std::atomic<int> g_launch_error{0};
-static void note_launch_error(cudaError_t e) {
+void note_launch_error(cudaError_t e) {
     int z = 0;
     g_launch_error.compare_exchange_strong(z, (int)e);
 }
@@ -4487,32 +4135,6 @@ cudaError_t last_error() {
     const cudaError_t e = (cudaError_t)g_launch_error.exchange(0);
     const cudaError_t g = cudaGetLastError();
     return e != cudaSuccess ? e : g;
-}
-
-// Launch with programmatic stream serialization (PDL) when PMG_PDL=1 (off by
-// default: no measurable gain inside the replayed cycle graph, r01).
-static bool pdl_on() {
-    static const bool on = [] {
-        const char* e = std::getenv("PMG_PDL");
-        return e ? std::atoi(e) != 0 : false;
-    }();
-    return on;
-}
-template <class... KArgs, class... Args>
-static void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                     Args&&... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = pdl_on() ? 1 : 0;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
-    if (e != cudaSuccess) note_launch_error(e);
 }
 
 int apply_launches(const LevelView& L) { return 1; }
@@ -4750,60 +4372,13 @@ static void radial_k(const LevelView& L, double* u, const double* f, const doubl
     launch_k(k_radial<ON, K>, dim3(lines, L.B), T, sm, st, L, u, f, ril, rm, parity, mode, active);
 }
 
-// rows per lane of the warp-per-line kernels for a line of n nodes when the
-// batch of lines_total concurrent lines is large enough (0: CTA-per-line
-// kernels).  PMG_WARP_LINES=0 disables; PMG_WARP_MIN_LINES sets the batch.
-static int warp_kw(int n, long lines_total) {
-    static const long min_lines = [] {
-        const char* e = std::getenv("PMG_WARP_MIN_LINES");
-        return e ? std::atol(e) : 2048L;
-    }();
-    static const bool on = [] {
-        const char* e = std::getenv("PMG_WARP_LINES");
-        return e ? std::atoi(e) != 0 : true;
-    }();
-    if (!on || lines_total < min_lines || n < 2) return 0;
-    const int ke = warp_ke(n);
-    return ke <= 3 ? 3 : ke <= 5 ? 5 : ke <= 9 ? 9 : ke <= 17 ? 17 : 0;
-}
-
-template <bool ON, int KW>
-static void radial_warp_k(const LevelView& L, double* u, const double* f, const double* ril,
-                          const double* rm, int parity, bool exact, const int* active,
-                          cudaStream_t st, long lines_total) {
-    constexpr int WPB = 4;  // warps (lines) per CTA
-    const size_t sm = (size_t)WPB * 3 * 32 * warp_ke(L.len) * sizeof(double);
-    const dim3 grid((unsigned)((lines_total + WPB - 1) / WPB));
-    if (exact) {
-        set_smem(k_radial_warp<ON, KW, true>, sm);
-        launch_k(k_radial_warp<ON, KW, true>, grid, 32 * WPB, sm, st, L, u, f, ril, rm, parity,
-                 active);
-    } else {
-        set_smem(k_radial_warp<ON, KW, false>, sm);
-        launch_k(k_radial_warp<ON, KW, false>, grid, 32 * WPB, sm, st, L, u, f, ril, rm, parity,
-                 active);
-    }
-}
-
 void launch_radial(const LevelView& L, bool onfly, double* u, const double* f, const double* ril,
                    const double* rm, int parity, bool serial, const int* active,
                    cudaStream_t st) {
     if (L.len <= 0) return;
     const int lines = (L.nt - parity + 1) / 2;
-    if (const int kw = warp_kw(L.len, (long)lines * L.B)) {
-        const long lt = (long)lines * L.B;
-#define PMG_RW(KK)                                                                         \
-    (onfly ? radial_warp_k<true, KK>(L, u, f, ril, rm, parity, serial, active, st, lt)     \
-           : radial_warp_k<false, KK>(L, u, f, ril, rm, parity, serial, active, st, lt))
-        switch (kw) {
-            case 3: PMG_RW(3); break;
-            case 5: PMG_RW(5); break;
-            case 9: PMG_RW(9); break;
-            default: PMG_RW(17); break;
-        }
-#undef PMG_RW
-        return;
-    }
+    if (launch_radial_tpl(L, onfly, u, f, ril, rm, parity, active, st)) return;
+    if (launch_radial_warp(L, onfly, u, f, ril, rm, parity, serial, active, st)) return;
     int K, T;
     static const int cl_min = [] {
         const char* e = std::getenv("PMG_RADIAL_CL_MIN");
@@ -5023,6 +4598,9 @@ void launch_set_active(int* active, int* count, int* conv, int* remaining, int B
     launch_k(k_set_active, (B + 127) / 128, 128, 0, st, active, count, conv, remaining, B);
 }
 
+void launch_loop_cond(cudaGraphConditionalHandle h, const int* remaining, cudaStream_t st) {
+    launch_k(k_loop_cond, 1, 32, 0, st, h, remaining);
+}
 void launch_flush(double* buf, long n, cudaStream_t st) {
     k_flush<<<148 * 8, 256, 0, st>>>(buf, n);
 }

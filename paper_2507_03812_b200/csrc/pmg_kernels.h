@@ -226,6 +226,15 @@ void launch_norm_check(const double* partials, int nblk, int B, long n, int norm
                        cudaStream_t st);
 
 void launch_fill(double* p, long n, double v, cudaStream_t st);
+// warp-per-line radial sweep (pmg_radial_warp.cu); false: not applicable
+bool launch_radial_warp(const LevelView& L, bool onfly, double* u, const double* f,
+                        const double* ril, const double* rm, int parity, bool serial,
+                        const int* active, cudaStream_t st);
+// thread-per-line radial sweep (pmg_tpl.cu); false: not applicable to this level / batch
+bool launch_radial_tpl(const LevelView& L, bool onfly, double* u, const double* f,
+                       const double* ril, const double* rm, int parity, const int* active,
+                       cudaStream_t st);
+void launch_loop_cond(cudaGraphConditionalHandle h, const int* remaining, cudaStream_t st);
 void launch_set_active(int* active, int* count, int* conv, int* remaining, int B,
                        cudaStream_t st);
 void launch_flush(double* buf, long n, cudaStream_t st);

@@ -227,6 +227,10 @@ struct Solver {
     int mprog_len[3] = {0, 0, 0};
     // CUDA graph of one cycle + residual norm + convergence check
     cudaGraphExec_t cycle_exec = nullptr;
+    // the whole iteration as ONE graph launch: a WHILE node whose body is the
+    // cycle graph and whose condition a device kernel sets from `remaining`
+    cudaGraphExec_t loop_exec = nullptr;
+    bool use_loop = true;
     long long cycle_nodes = 0;
     bool use_graph = true;
     int* h_remaining = nullptr;
@@ -256,6 +260,7 @@ struct Solver {
         }
         for (auto e : ev_pool) cudaEventDestroy(e);
         if (cycle_exec) cudaGraphExecDestroy(cycle_exec);
+        if (loop_exec) cudaGraphExecDestroy(loop_exec);
         for (void* p : allocs) cudaFree(p);
         if (h_remaining) cudaFreeHost(h_remaining);
         if (own_stream && stream) cudaStreamDestroy(stream);
@@ -1209,6 +1214,62 @@ struct Solver {
         launches = l0;
     }
 
+    // The solve loop of multigrid.cpp:328-340 on the device: a conditional
+    // WHILE node replays {cycle, residual norm, convergence check, condition}
+    // until no section is iterating -- no host round trip between cycles.
+    // Falls back to the per-cycle graph launches (host loop) if the driver
+    // rejects the conditional graph.
+    bool build_loop_graph() {
+        const long long l0 = launches;
+        cudaGraph_t g = nullptr;
+        bool ok = cudaGraphCreate(&g, 0) == cudaSuccess;
+        cudaGraphConditionalHandle h{};
+        ok = ok && cudaGraphConditionalHandleCreate(&h, g, 0, 0) == cudaSuccess;
+        cudaGraphNode_t first = nullptr;
+        if (ok) {  // condition of the first pass, from the initial norm check
+            cudaGraph_t tmp = nullptr;
+            ok = cudaStreamBeginCaptureToGraph(stream, g, nullptr, nullptr, 0,
+                                               cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+            if (ok) {
+                launch_loop_cond(h, remaining, stream);
+                ok = cudaStreamEndCapture(stream, &tmp) == cudaSuccess;
+            }
+            size_t nn = 1;
+            ok = ok && cudaGraphGetNodes(g, &first, &nn) == cudaSuccess && nn == 1;
+        }
+        if (ok) {
+            cudaGraphNodeParams cp{};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = h;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            cudaGraphNode_t wn = nullptr;
+            ok = cudaGraphAddNode(&wn, g, &first, 1, &cp) == cudaSuccess;
+            if (ok) {
+                cudaGraph_t body = cp.conditional.phGraph_out[0], tmp = nullptr;
+                ok = cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0,
+                                                   cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+                if (ok) {
+                    cycle(0, set.cycle, act_mask());
+                    norm_check();
+                    launch_loop_cond(h, remaining, stream);
+                    ok = cudaStreamEndCapture(stream, &tmp) == cudaSuccess;
+                }
+            }
+        }
+        ok = ok && cudaGraphInstantiate(&loop_exec, g, 0) == cudaSuccess;
+        if (g) cudaGraphDestroy(g);
+        cycle_nodes = launches - l0;
+        launches = l0;
+        if (!ok) {
+            cudaGetLastError();
+            last_error();
+            loop_exec = nullptr;
+            use_loop = false;
+        }
+        return ok;
+    }
+
     // PMG_TAIL_TRACE: per-op durations of the last coarse-tail launch (stderr)
     void print_tail_trace() {
         const std::vector<int>& prog = h_prog[set.cycle];
@@ -1379,9 +1440,18 @@ struct Solver {
         }
         norm_check();
         const bool graph = use_graph && !prof;
-        if (graph && !cycle_exec) build_cycle_graph();
+        bool looped = false;
+        if (const char* e = std::getenv("PMG_LOOP_GRAPH")) use_loop = use_loop && std::atoi(e) != 0;
+        if (graph && use_loop && !set.verbose) {
+            if (!loop_exec) build_loop_graph();
+            if (loop_exec) {
+                PMG_CUDA(cudaGraphLaunch(loop_exec, stream));
+                looped = true;
+            }
+        }
+        if (graph && !looped && !cycle_exec) build_cycle_graph();
         int it = 0;
-        for (;;) {
+        for (; !looped;) {
             PMG_CUDA(cudaMemcpyAsync(h_remaining, remaining, sizeof(int), cudaMemcpyDeviceToHost,
                                      stream));
             PMG_CUDA(cudaStreamSynchronize(stream));
@@ -1415,6 +1485,7 @@ struct Solver {
         std::vector<int> h_it(B), h_conv(B);
         std::vector<double> h_hist((size_t)B * hist_cap);
         PMG_CUDA(cudaMemcpy(h_it.data(), iters, sizeof(int) * B, cudaMemcpyDeviceToHost));
+        if (looped) launches += cycle_nodes * *std::max_element(h_it.begin(), h_it.end());
         PMG_CUDA(cudaMemcpy(h_conv.data(), conv, sizeof(int) * B, cudaMemcpyDeviceToHost));
         PMG_CUDA(cudaMemcpy(h_hist.data(), hist, sizeof(double) * h_hist.size(),
                             cudaMemcpyDeviceToHost));
