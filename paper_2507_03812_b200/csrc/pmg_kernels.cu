@@ -128,11 +128,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 
 // loads of u inside a launch whose other CTAs write u (fused smoothing) go
 // through L2 (ld.global.cg): L1 is not coherent across SMs
-template <bool CG>
-__device__ __forceinline__ double ldu(const double* p) {
-    if (CG) return __ldcg(p);
-    return *p;
-}
 __device__ __forceinline__ int P(int i) { return i + (i >> 4); }  // bank-conflict padding
 __host__ __device__ __forceinline__ int padded(int n) { return n + (n >> 4) + 1; }
 
@@ -1093,43 +1088,6 @@ __device__ void origin_solve_serial(double* Y, double* X, const OriginFactor& of
         if (i >= 1) X[i - 1] -= b1[i] * xi;
     }
     for (int k = 0; k < n; ++k) Y[P((k & 1) ? h + (k >> 1) : (k >> 1))] = X[k];
-}
-
-// Circle-line rhs (smoother.cpp:162-182) of an interior Take ring: rings
-// s-1, s+1 are circle rings and not Dirichlet, so the off-line couplings are
-// the row_from expressions with has_sm = has_sp = true (same values).
-__device__ __forceinline__ bool circle_lean_ring(const LevelView& L, int s) {
-#ifdef PMG_NO_CIRCLE_LEAN
-    return false;
-#endif
-    return s >= 1 && s + 1 < L.split && s + 1 < L.nr - 1 && !(s == 1 && L.boundary == 1);
-}
-template <bool CG = false>
-__device__ __forceinline__ double circle_rhs_lean(const LevelView& L, long off, int s, int t,
-                                                  const double* __restrict__ U,
-                                                  const double* __restrict__ F) {
-    const int nt = L.nt, p = s * nt + t;
-    const int tm = t == 0 ? nt - 1 : t - 1, tp = t + 1 == nt ? 0 : t + 1;
-    const int pTM = s * nt + tm, pTP = s * nt + tp;
-    const double* A = L.arr + off;
-    const double* R = L.art + off;
-    const double aP = A[p], aSM = A[p - nt], aSP = A[p + nt];
-    const double rTM = R[pTM], rTP = R[pTP], rSM = R[p - nt], rSP = R[p + nt];
-    const double uSM = ldu<CG>(&U[p - nt]), uSP = ldu<CG>(&U[p + nt]);
-    const double uSMTM = ldu<CG>(&U[pTM - nt]), uSMTP = ldu<CG>(&U[pTP - nt]);
-    const double uSPTM = ldu<CG>(&U[pTM + nt]), uSPTP = ldu<CG>(&U[pTP + nt]);
-    const double fP = F[p];
-    const double kbar = 0.5 * (L.k[tm] + L.k[t]);
-    const double qkm = xdiv(kbar, L.h[s - 1], L.rh[s - 1]);
-    const double qkp = xdiv(kbar, L.h[s], L.rh[s]);
-    double acc = fP;
-    acc -= (-qkm * (aP + aSM)) * uSM;
-    acc -= (-qkp * (aP + aSP)) * uSP;
-    acc -= (-(rTM + rSM) * 0.25) * uSMTM;
-    acc -= ((rSM + rTP) * 0.25) * uSMTP;
-    acc -= ((rTM + rSP) * 0.25) * uSPTM;
-    acc -= (-(rSP + rTP) * 0.25) * uSPTP;
-    return acc;
 }
 
 // ------------------------------------------------------------ apply / residual
@@ -4268,10 +4226,62 @@ void launch_circle(const LevelView& L, bool onfly, double* u, const double* f, c
                    const double* cm, const double* corner, const double* cz,
                    const OriginFactor& of, int parity, bool serial, int exact_rings,
                    const int* active, cudaStream_t st) {
-    const int lines = L.split > parity ? (L.split - parity + 1) / 2 : 0;
+    int lines = L.split > parity ? (L.split - parity + 1) / 2 : 0;
     if (lines == 0) return;
-    const int C = (!serial && exact_rings <= 0) ? line_cluster(L.nt) : 1;
     int K, T;
+    // large batches of Take lines: one warp per ring (pmg_radial_warp.cu); the
+    // across-origin ring, which is not a cyclic line, by the CTA kernel
+    if (!onfly && !L.rows && exact_rings <= 0) {
+        const bool org = parity == 0 && L.boundary == 0;
+        const int s_first = org ? 2 : parity;
+        const int nl = L.split > s_first ? (L.split - s_first + 1) / 2 : 0;
+        // (fast mode keeps the CTA kernels: their two-rhs scans are quicker there)
+        cudaStream_t side = st;
+        cudaEvent_t fork = nullptr, join = nullptr;
+        if (serial && org && nl > 0 && warp_batch_ok(L.nt, (long)nl * L.B)) {
+            // ring 0 on a side stream, forked from / joined back into st: it
+            // overlaps the other rings (a parallel branch of the cycle graph)
+            static thread_local cudaStream_t s_side[64] = {};
+            static thread_local cudaEvent_t s_fork[64] = {}, s_join[64] = {};
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (!s_side[dev]) {
+                cudaStreamCreateWithFlags(&s_side[dev], cudaStreamNonBlocking);
+                cudaEventCreateWithFlags(&s_fork[dev], cudaEventDisableTiming);
+                cudaEventCreateWithFlags(&s_join[dev], cudaEventDisableTiming);
+            }
+            side = s_side[dev];
+            fork = s_fork[dev];
+            join = s_join[dev];
+            cudaEventRecord(fork, st);
+            cudaStreamWaitEvent(side, fork, 0);
+        }
+        if (serial && nl > 0 &&
+            launch_circle_warp(L, u, f, cil, cm, corner, cz, s_first, nl, serial, active, st)) {
+            if (!org) return;
+            struct Join {
+                cudaStream_t st, side;
+                cudaEvent_t join;
+                ~Join() {
+                    if (join) {
+                        cudaEventRecord(join, side);
+                        cudaStreamWaitEvent(st, join, 0);
+                    }
+                }
+            } joiner{st, side, join};
+            st = side;
+            lines = 1;  // ring 0 below
+            line_shape(L.nt, K, T, (long)L.B);
+            switch (K) {
+                case 2: circle_k<false, 2>(L, u, f, cil, cm, corner, cz, of, 0, serial, exact_rings, active, st, T, 1); break;
+                case 4: circle_k<false, 4>(L, u, f, cil, cm, corner, cz, of, 0, serial, exact_rings, active, st, T, 1); break;
+                case 8: circle_k<false, 8>(L, u, f, cil, cm, corner, cz, of, 0, serial, exact_rings, active, st, T, 1); break;
+                default: circle_k<false, 16>(L, u, f, cil, cm, corner, cz, of, 0, serial, exact_rings, active, st, T, 1); break;
+            }
+            return;
+        }
+    }
+    const int C = (!serial && exact_rings <= 0) ? line_cluster(L.nt) : 1;
     if (C > 1) {
         int s_first = parity, nl = lines;
         // the across-origin ring runs as a single-CTA kernel on a side stream,

@@ -230,6 +230,12 @@ void launch_fill(double* p, long n, double v, cudaStream_t st);
 bool launch_radial_warp(const LevelView& L, bool onfly, double* u, const double* f,
                         const double* ril, const double* rm, int parity, bool serial,
                         const int* active, cudaStream_t st);
+// whether a batch of lines_total lines of n nodes runs on the warp-per-line kernels
+bool warp_batch_ok(int n, long lines_total);
+// warp-per-line circle sweep of rings s_first, s_first + 2, ... (nl rings, not the origin ring)
+bool launch_circle_warp(const LevelView& L, double* u, const double* f, const double* cil,
+                        const double* cm, const double* corner, const double* cz, int s_first,
+                        int nl, bool serial, const int* active, cudaStream_t st);
 // thread-per-line radial sweep (pmg_tpl.cu); false: not applicable to this level / batch
 bool launch_radial_tpl(const LevelView& L, bool onfly, double* u, const double* f,
                        const double* ril, const double* rm, int parity, const int* active,

@@ -167,6 +167,74 @@ __device__ __forceinline__ void warp_scan(double A, double (&B)[NV], double (&yi
 }
 
 
+template <bool CG>
+__device__ __forceinline__ double ldu(const double* p) {
+    if (CG) return __ldcg(p);
+    return *p;
+}
+
+// Circle-line rhs (smoother.cpp:162-182) of an interior Take ring: rings
+// s-1, s+1 are circle rings and not Dirichlet, so the off-line couplings are
+// the row_from expressions with has_sm = has_sp = true (same values).
+__device__ __forceinline__ bool circle_lean_ring(const LevelView& L, int s) {
+#ifdef PMG_NO_CIRCLE_LEAN
+    return false;
+#endif
+    return s >= 1 && s + 1 < L.split && s + 1 < L.nr - 1 && !(s == 1 && L.boundary == 1);
+}
+struct CircOps {  // operands of one node of a lean ring
+    double aP, aSM, aSP, rTM, rTP, rSM, rSP, uSM, uSP, uSMTM, uSMTP, uSPTM, uSPTP, fP, km, kp;
+};
+template <bool CG = false>
+__device__ __forceinline__ void circ_load(const LevelView& L, long off, int s, int t,
+                                          const double* __restrict__ U,
+                                          const double* __restrict__ F, CircOps& o) {
+    const int nt = L.nt, p = s * nt + t;
+    const int tm = t == 0 ? nt - 1 : t - 1, tp = t + 1 == nt ? 0 : t + 1;
+    const int pTM = s * nt + tm, pTP = s * nt + tp;
+    const double* A = L.arr + off;
+    const double* R = L.art + off;
+    o.aP = A[p];
+    o.aSM = A[p - nt];
+    o.aSP = A[p + nt];
+    o.rTM = R[pTM];
+    o.rTP = R[pTP];
+    o.rSM = R[p - nt];
+    o.rSP = R[p + nt];
+    o.uSM = ldu<CG>(&U[p - nt]);
+    o.uSP = ldu<CG>(&U[p + nt]);
+    o.uSMTM = ldu<CG>(&U[pTM - nt]);
+    o.uSMTP = ldu<CG>(&U[pTP - nt]);
+    o.uSPTM = ldu<CG>(&U[pTM + nt]);
+    o.uSPTP = ldu<CG>(&U[pTP + nt]);
+    o.fP = F[p];
+    o.km = L.k[tm];
+    o.kp = L.k[t];
+}
+// hm, rhm, hp, rhp: h_{s-1}, RN(1/h_{s-1}), h_s, RN(1/h_s)
+__device__ __forceinline__ double circ_eval(const CircOps& o, double hm, double rhm, double hp,
+                                            double rhp) {
+    const double kbar = 0.5 * (o.km + o.kp);
+    const double qkm = xdiv(kbar, hm, rhm);
+    const double qkp = xdiv(kbar, hp, rhp);
+    double acc = o.fP;
+    acc -= (-qkm * (o.aP + o.aSM)) * o.uSM;
+    acc -= (-qkp * (o.aP + o.aSP)) * o.uSP;
+    acc -= (-(o.rTM + o.rSM) * 0.25) * o.uSMTM;
+    acc -= ((o.rSM + o.rTP) * 0.25) * o.uSMTP;
+    acc -= ((o.rTM + o.rSP) * 0.25) * o.uSPTM;
+    acc -= (-(o.rSP + o.rTP) * 0.25) * o.uSPTP;
+    return acc;
+}
+template <bool CG = false>
+__device__ __forceinline__ double circle_rhs_lean(const LevelView& L, long off, int s, int t,
+                                                  const double* __restrict__ U,
+                                                  const double* __restrict__ F) {
+    CircOps o;
+    circ_load<CG>(L, off, s, t, U, F, o);
+    return circ_eval(o, L.h[s - 1], L.rh[s - 1], L.h[s], L.rh[s]);
+}
+
 // Opt a kernel into the full 227 KB of dynamic shared memory once per
 // (kernel, device); launches then pass their exact size.
 template <class KernelT>

@@ -242,6 +242,101 @@ __global__ void __launch_bounds__(128) k_radial_warp(LevelView L, double* __rest
     for (int i = lane; i < len; i += 32) U[base + i] = Y[i];
 }
 
+// ---------------------------------------------- warp-per-line circle sweep
+// The same scheme for large batches of circle lines (config 3: 10496 rings of
+// 512 nodes per colour): one warp per ring, rhs gather (smoother.cpp:162-182;
+// lean interior rings branch-free with the operands of kRadUnroll nodes in
+// flight per lane, the ring next to the radial region through the general
+// row), the core solve T y = b by warp_tri on the identity-padded line, then
+// the Sherman-Morrison correction of cyclic_tridiag_solve
+// (line_algebra.cpp:112-118) with the precomputed z = T^{-1}(e_1 + e_n)
+// (k_circle_z, the reference's own sequence).  The across-origin ring is not
+// a cyclic line and stays with k_circle.
+template <int KE, bool EXACT>
+__global__ void __launch_bounds__(128) k_circle_warp(LevelView L, double* __restrict__ u,
+                                                     const double* __restrict__ f,
+                                                     const double* __restrict__ cil,
+                                                     const double* __restrict__ cm,
+                                                     const double* __restrict__ corner,
+                                                     const double* __restrict__ cz, int s_first,
+                                                     int nl, const int* __restrict__ active) {
+    pdl_enter();
+    extern __shared__ double smem[];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const long g = (long)blockIdx.x * (blockDim.x >> 5) + w;
+    if (g >= (long)nl * L.B) return;  // whole warps only
+    const int b = (int)(g / nl);
+    const int s = s_first + 2 * (int)(g - (long)b * nl);
+    if (active && !active[b]) return;
+    constexpr int stride = 32 * KE;
+    const int nt = L.nt;
+    const long off = (long)b * L.n;
+    double* U = u + off;
+    const double* F = f + off;
+    const int base = s * nt;
+    if (L.dir(s)) {
+        for (int t = lane; t < nt; t += 32) U[base + t] = F[base + t];
+        return;
+    }
+    const long fo = (long)b * L.split * nt + (long)s * nt;
+    double* Y = smem + (long)w * warp_slice(KE);
+    double* Ld = Y + stride;
+    double* Mp = Ld + stride;  // stride + 1 entries
+#pragma unroll 4
+    for (int i = lane; i < stride; i += 32) {
+        Ld[i] = i < nt ? cil[fo + i] : 1.0;
+        Mp[i + 1] = i < nt - 1 ? cm[fo + i] : 0.0;
+        if (i >= nt) Y[i] = 0.0;
+    }
+    if (lane == 0) Mp[0] = 0.0;
+    if (circle_lean_ring(L, s)) {
+        const double hm = L.h[s - 1], rhm = L.rh[s - 1], hp = L.h[s], rhp = L.rh[s];
+        for (int t0 = lane; t0 < nt; t0 += 32 * kRadUnroll) {
+            CircOps o[kRadUnroll];
+#pragma unroll
+            for (int q = 0; q < kRadUnroll; ++q)
+                if (t0 + 32 * q < nt) circ_load<false>(L, off, s, t0 + 32 * q, U, F, o[q]);
+#pragma unroll
+            for (int q = 0; q < kRadUnroll; ++q)
+                if (t0 + 32 * q < nt) Y[t0 + 32 * q] = circ_eval(o[q], hm, rhm, hp, rhp);
+        }
+    } else {
+        const CoefAt<false> cf{&L, off, b};
+        for (int t = lane; t < nt; t += 32) {
+            const int p = base + t;
+            const Nbr q = neighbours(L, s, t, p);
+            const Row R = make_row_fast(L, cf, s, t, p, q);
+            double acc = F[p];
+            if (R.has_sm) acc -= R.sm * U[q.pSM];
+            if (R.has_sp) acc -= R.sp * U[q.pSP];
+            if (R.has_sm) {
+                acc -= R.mm * U[q.pSMTM];
+                acc -= R.mp * U[q.pSMTP];
+            }
+            if (R.has_sp) {
+                acc -= R.pm * U[q.pSPTM];
+                acc -= R.pp * U[q.pSPTP];
+            }
+            Y[t] = acc;
+        }
+    }
+    __syncwarp();
+    const int j0 = lane * KE;
+    double y[KE];
+#pragma unroll
+    for (int q = 0; q < KE; ++q) y[q] = Y[j0 + q];
+    warp_tri<KE, EXACT>(y, Ld, Mp);
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < KE; ++q) Y[j0 + q] = y[q];
+    __syncwarp();
+    // tau = c (x_0 + x_{n-1}) / (1 + c (z_0 + z_{n-1})); x -= tau z
+    const double c = corner[(long)b * L.split + s];
+    const double* __restrict__ z = cz + fo;
+    const double tau = c * (Y[0] + Y[nt - 1]) / (1.0 + c * (z[0] + z[nt - 1]));
+    for (int t = lane; t < nt; t += 32) U[base + t] = Y[t] - tau * z[t];
+}
+
 }  // namespace
 
 // rows per lane of the warp-per-line kernels for a line of n nodes when the
@@ -309,6 +404,50 @@ bool launch_radial_warp(const LevelView& L, bool onfly, double* u, const double*
         return true;
     }
     return false;
+}
+
+
+bool warp_batch_ok(int n, long lines_total) { return warp_kw(n, lines_total) != 0; }
+
+template <int KW>
+static void circle_warp_k(const LevelView& L, double* u, const double* f, const double* cil,
+                          const double* cm, const double* corner, const double* cz, int s_first,
+                          int nl, bool exact, const int* active, cudaStream_t st) {
+    constexpr int WPB = 4;  // warps (lines) per CTA
+    const size_t sm = (size_t)WPB * warp_slice(KW) * sizeof(double);
+    const dim3 grid((unsigned)(((long)nl * L.B + WPB - 1) / WPB));
+    if (exact) {
+        set_smem(k_circle_warp<KW, true>, sm);
+        launch_k(k_circle_warp<KW, true>, grid, 32 * WPB, sm, st, L, u, f, cil, cm, corner, cz,
+                 s_first, nl, active);
+    } else {
+        set_smem(k_circle_warp<KW, false>, sm);
+        launch_k(k_circle_warp<KW, false>, grid, 32 * WPB, sm, st, L, u, f, cil, cm, corner, cz,
+                 s_first, nl, active);
+    }
+}
+
+// Rings s_first, s_first + 2, ... (nl of them, none the across-origin ring) of
+// a Take level with cached coefficients; false: batch too small / lines too long.
+bool launch_circle_warp(const LevelView& L, double* u, const double* f, const double* cil,
+                        const double* cm, const double* corner, const double* cz, int s_first,
+                        int nl, bool serial, const int* active, cudaStream_t st) {
+    if (L.rows || !cz) return false;
+    const int kw = warp_kw(L.nt, (long)nl * L.B);
+    if (!kw) return false;
+#define PMG_CW(KK) circle_warp_k<KK>(L, u, f, cil, cm, corner, cz, s_first, nl, serial, active, st)
+    switch (kw) {
+        case 1: case 3: PMG_CW(3); break;
+        case 5: PMG_CW(5); break;
+        case 7: PMG_CW(7); break;
+        case 9: PMG_CW(9); break;
+        case 11: PMG_CW(11); break;
+        case 13: PMG_CW(13); break;
+        case 15: PMG_CW(15); break;
+        default: PMG_CW(17); break;
+    }
+#undef PMG_CW
+    return true;
 }
 
 }  // namespace pmg
