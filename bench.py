@@ -49,6 +49,7 @@ WORKLOADS = {
     "c2w": (2, "Czarny 4097x4096 Take W(1,1) rel 1e-10"),
     "c3": (3, "256 x Shafranov 513x512 Take V(1,1) rel 1e-10, alpha*U(0.5,2)"),
     "c4": (4, "Czarny 8193x8192 Take kernel microbench"),
+    "give": (2, "Czarny 4097x4096 Give kernel microbench"),
 }
 
 # algorithmic bytes per node of one launch
@@ -246,8 +247,9 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     wl = args.workload
-    if wl == "c4":
-        print(json.dumps({"impl": "reference", "unavailable": "c4 is a kernel microbench; use c3"}))
+    if wl in ("c4", "give"):
+        print(json.dumps({"impl": "reference",
+                          "unavailable": f"{wl} is a kernel microbench; use c3"}))
         return 0
     threads = os.cpu_count() or 1
     per_step = []
@@ -331,6 +333,8 @@ def run_gpu(args):
 
     if args.workload == "c4":
         return run_c4(args, rank, world, local, stream, peak, peak_kind, dist)
+    if args.workload == "give":
+        return run_give(args, rank, world, local, stream, peak, peak_kind, dist)
 
     solver, sections = build_solver(args.workload, rank, world, stream.cuda_stream,
                                     not args.fast, device=local)
@@ -514,11 +518,63 @@ def kernel_roofline(solver, kind, peak, peak_kind, reps=20, workload=None):
             "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"}
 
 
+# Give mode (stencil.cpp:176-287 recast as a gather): coefficients are
+# re-evaluated on the fly, so a launch moves only u, f and the result (24 B per
+# node); the sweeps also read their two factor bands (40 B).  The
+# FP64 operations per node are counted by ncu (smsp__sass_thread_inst_executed_
+# op_d{fma,mul,add}_pred_on of the captures under profiles/; 2 flops per DFMA)
+# and reported against the B200's FP64 vector peak next to the HBM fraction.
+GIVE_BYTES = {"residual": 24.0, "circle": 40.0, "radial": 40.0}
+FP64_PEAK_TFLOPS = 37.0  # datasheet FP64 (non-tensor) peak; not in MEASURED_PEAKS.json
+
+
+def run_give(args, rank, world, local, stream, peak, peak_kind, dist):
+    """Give-operator roofline at 4097x4096: residual,
+    circle sweep B+W and radial sweep B+W against HBM and FP64 peak."""
+    import paper_2507_03812_b200 as pmg
+    geom, prob, grid, st, meta = pmg.baseline_config(2, stencil_mode="Give",
+                                                     reference_order=not args.fast)
+    solver = pmg.MultigridSolver(geom, prob, grid, st, device=local, stream=stream.cuda_stream)
+    n = solver.n(0)
+    nr, nt, split = solver.level_shape(0)
+    rng = np.random.default_rng(SEED)
+    solver.residual(rng.uniform(-1, 1, n), rng.uniform(-1, 1, n), 0)
+    try:
+        with open(os.path.join(ROOT, "profiles", "give_flops.json")) as fh:
+            flops = json.load(fh)
+    except Exception:
+        flops = {}
+    out = {}
+    for k in ("residual", "circle", "radial"):
+        nodes = {"residual": nr * nt, "circle": split * nt, "radial": (nr - split) * nt}[k]
+        ms = solver.time_kernel(k, 0, args.reps, True)
+        gbs = GIVE_BYTES[k] * nodes / (ms * 1e-3) / 1e9
+        fl = flops.get(k)  # FP64 flops per node (ncu)
+        out[k] = {"kernel": f"Give {k} (finest level{'' if k == 'residual' else ', B+W'})",
+                  "ms_per_launch": round(ms, 5), "bytes_per_node": GIVE_BYTES[k],
+                  "hbm": {"achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
+                          "frac": round(gbs / peak, 4)},
+                  "fp64": None if fl is None else {
+                      "flops_per_node": fl, "achieved": round(fl * nodes / (ms * 1e-3) / 1e12, 2),
+                      "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                      "frac": round(fl * nodes / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4)}}
+    if rank == 0:
+        print(json.dumps({"metric": "Give residual/smoother GB/s and FP64 TFLOP/s (4097x4096)",
+                          "value": out["residual"]["hbm"]["achieved"], "unit": "GB/s",
+                          "n_gpus": world, "steps": args.reps, "warmup": 0,
+                          "higher_is_better": True, "dtype": "f64",
+                          "config": {"workload": "give: " + WORKLOADS["give"][1],
+                                     "grid": "4097x4096",
+                                     "l2": "flushed before every repetition"},
+                          "kernels": out}))
+    return 0
+
+
 def run_c4(args, rank, world, local, stream, peak, peak_kind, dist):
     """Config 4 roofline microbench: 100 reps of the Take residual, circle
     sweep B+W and radial sweep B+W on seeded U(-1,1) iterates."""
     import paper_2507_03812_b200 as pmg
-    geom, prob, grid, st, meta = pmg.baseline_config(4)
+    geom, prob, grid, st, meta = pmg.baseline_config(4, reference_order=not args.fast)
     solver = pmg.MultigridSolver(geom, prob, grid, st, device=local, stream=stream.cuda_stream)
     n = solver.n(0)
     rng = np.random.default_rng(SEED)
@@ -535,7 +591,9 @@ def run_c4(args, rank, world, local, stream, peak, peak_kind, dist):
                 "value": out["radial"]["achieved"], "unit": "GB/s", "n_gpus": world,
                 "steps": reps, "warmup": 0, "higher_is_better": True, "dtype": "f64",
                 "config": {"workload": "c4: " + WORKLOADS["c4"][1], "grid": "8193x8192",
-                           "l2": "flushed before every repetition"},
+                           "l2": "flushed before every repetition",
+                           "line_solves": "chunked scans (fast)" if args.fast
+                           else "reference order (bitwise)"},
                 "kernels": out}
         print(json.dumps(line))
     return 0

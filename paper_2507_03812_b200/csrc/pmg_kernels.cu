@@ -576,24 +576,32 @@ __device__ void tri_solve_exact(double* Y, const double* Ld, const double* M, in
 // Branch-free (selects, clamped indices): the rows of a chunk unroll into
 // straight-line code whose shared-memory loads the scheduler hoists ahead of
 // the dependent DMUL-DADD-DMUL-DFMA-DFMA chain.
+// RCF: RN(1/l) evaluated on the fly (lines whose four arrays do not fit one
+// CTA's shared memory keep three); it is off the dependency chain either way
+template <bool RCF>
+__device__ __forceinline__ double rc_at(const double* Ld, const double* RC, int j) {
+    return RCF ? __drcp_rn(Ld[P(j)]) : RC[P(j)];
+}
+template <bool RCF = false>
 __device__ __forceinline__ double ex_fwd(const double* Y, const double* Ld, const double* RC,
                                          const double* M, int j, double v) {
     const double b = Y[P(j)];
     const double m = M[P(j > 0 ? j - 1 : 0)];
     const double a = b - m * v;
-    return xdiv(j == 0 ? b : a, Ld[P(j)], RC[P(j)]);
+    return xdiv(j == 0 ? b : a, Ld[P(j)], rc_at<RCF>(Ld, RC, j));
 }
 // backward row j of L^T x = y, v = x_{j+1}; yj = y_j
+template <bool RCF = false>
 __device__ __forceinline__ double ex_bwd(double yj, const double* Ld, const double* RC,
                                          const double* M, int n, int j, double v) {
     const double a = yj - M[P(j)] * v;
-    return xdiv(j == n - 1 ? yj : a, Ld[P(j)], RC[P(j)]);
+    return xdiv(j == n - 1 ? yj : a, Ld[P(j)], rc_at<RCF>(Ld, RC, j));
 }
 
 // KS rows per solving thread (independent of the kernel's chunk K: threads
 // t >= ceil(n/KS) idle in the solve); warm-up = one chunk.  Each wave costs
 // one barrier: the chunk results are double-buffered.
-template <int KS, bool CYC>
+template <int KS, bool CYC, bool RCF = false>
 __device__ __forceinline__ void line_solve_ex(double* Y, const double* Ld, const double* RC,
                                               const double* M, int n, double corner,
                                               const double* __restrict__ z, double* scr) {
@@ -610,7 +618,7 @@ __device__ __forceinline__ void line_solve_ex(double* Y, const double* Ld, const
         for (int q = 0; q < KS; ++q) {
             const int j = j0 + q;
             if (j < n) {
-                const double il = RC[P(j)];
+                const double il = rc_at<RCF>(Ld, RC, j);
                 const double a = j > 0 ? -(M[P(j - 1)] * il) : 0.0;
                 Bv[0] = a * Bv[0] + Y[P(j)] * il;
                 A = a * A;
@@ -624,7 +632,7 @@ __device__ __forceinline__ void line_solve_ex(double* Y, const double* Ld, const
         if (live && t >= 1) {
             double v = t >= 2 ? Sa[t - 1] : 0.0;  // thread 1 restarts at row 0: exact
 #pragma unroll
-            for (int q = 0; q < KS; ++q) v = ex_fwd(Y, Ld, RC, M, j0 - KS + q, v);
+            for (int q = 0; q < KS; ++q) v = ex_fwd<RCF>(Y, Ld, RC, M, j0 - KS + q, v);
             st = v;
         }
         // rows past n (last chunk) recompute row n-1 and are never stored;
@@ -633,7 +641,7 @@ __device__ __forceinline__ void line_solve_ex(double* Y, const double* Ld, const
 #pragma unroll
             for (int q = 0; q < KS; ++q) {
                 const int j = min(j0 + q, n - 1);
-                const double w = ex_fwd(Y, Ld, RC, M, j, v);
+                const double w = ex_fwd<RCF>(Y, Ld, RC, M, j, v);
                 v = j0 + q < n ? w : v;
                 y[q] = v;
             }
@@ -665,7 +673,7 @@ __device__ __forceinline__ void line_solve_ex(double* Y, const double* Ld, const
         for (int q = KS - 1; q >= 0; --q) {
             const int j = j0 + q;
             if (j < n) {
-                const double il = RC[P(j)];
+                const double il = rc_at<RCF>(Ld, RC, j);
                 const double g = j < n - 1 ? -(M[P(j)] * il) : 0.0;
                 Dv[0] = g * Dv[0] + y[q] * il;
                 G = g * G;
@@ -684,7 +692,7 @@ __device__ __forceinline__ void line_solve_ex(double* Y, const double* Ld, const
 #pragma unroll
             for (int q = KS - 1; q >= 0; --q) {
                 const int j = min(j0 + KS + q, n - 1);
-                const double w = ex_bwd(Y[P(j)], Ld, RC, M, n, j, v);
+                const double w = ex_bwd<RCF>(Y[P(j)], Ld, RC, M, n, j, v);
                 v = j0 + KS + q < n ? w : v;
             }
             st = v;
@@ -694,7 +702,7 @@ __device__ __forceinline__ void line_solve_ex(double* Y, const double* Ld, const
 #pragma unroll
             for (int q = KS - 1; q >= 0; --q) {
                 const int j = min(j0 + q, n - 1);
-                const double w = ex_bwd(Y[P(j)], Ld, RC, M, n, j, v);
+                const double w = ex_bwd<RCF>(Y[P(j)], Ld, RC, M, n, j, v);
                 v = j0 + q < n ? w : v;
                 y[q] = v;
             }
@@ -1990,6 +1998,9 @@ __device__ __forceinline__ void circle_body(const LevelView& L, double* __restri
         KT(3);
         if (exact && par_ex)
             line_solve_ex<kExChunk, true>(Y, IL, RC, M, nt, corner[(long)b * L.split + s], cz + fo, scr);
+        else if (serial == 3)
+            line_solve_ex<kExChunk, true, true>(Y, IL, nullptr, M, nt, corner[(long)b * L.split + s],
+                                                cz + fo, scr);
         else if (exact)
             cyc_solve_exact(Y, IL, M, nt, corner[(long)b * L.split + s], cz + fo, scr);
         else
@@ -2142,6 +2153,8 @@ __device__ __forceinline__ void radial_body(const LevelView& L, double* __restri
     KT(3);
     if (serial == 1) {
         line_solve_ex<kExChunk, false>(Y, IL, RC, M, len, 0.0, nullptr, scr);
+    } else if (serial == 3) {
+        line_solve_ex<kExChunk, false, true>(Y, IL, nullptr, M, len, 0.0, nullptr, scr);
     } else if (serial) {
         if (threadIdx.x == 0) tri_solve_exact(Y, IL, M, len);
         __syncthreads();
@@ -4072,13 +4085,20 @@ inline void line_shape(int n, int& K, int& T, long lines_total = 0) {
 
 // shared memory of a single-CTA line: Y, IL, M (+ RC and the chunk tables of
 // the exact-order parallel solve when ex4)
-inline size_t line_smem(int n, bool ex4 = false, int T = 512) {
+inline size_t line_smem(int n, bool ex4 = false, int T = 512, bool ex3 = false) {
+    if (ex3) return (size_t)(3 * padded(n) + 64 + 3 * T) * sizeof(double);
     return ex4 ? (size_t)(4 * padded(n) + 64 + 6 * T) * sizeof(double)
                : (size_t)(3 * padded(n) + 32 * 6 + 16) * sizeof(double);
 }
 // line-solve mode of an exact (reference_order) solve: 1 = parallel exact
 // (line_solve_ex) when its four line arrays fit one CTA, else 2 = one thread
-inline int exact_mode(int n) { return line_smem(n, true) <= 227 * 1024 ? 1 : 2; }
+// (line_solve_ex), 3 = the same with RN(1/l) evaluated on the fly (three line
+// arrays: 8192-node lines), 2 = one thread
+inline int exact_mode(int n) {
+    return line_smem(n, true) <= 227 * 1024                 ? 1
+           : line_smem(n, false, 512, true) <= 227 * 1024 ? 3
+                                                          : 2;
+}
 
 }  // namespace
 
@@ -4165,7 +4185,7 @@ static void circle_k(const LevelView& L, double* u, const double* f, const doubl
                      const OriginFactor& of, int parity, bool serial, int exact_rings,
                      const int* active, cudaStream_t st, int T, int lines) {
     const int mode = serial ? exact_mode(L.nt) : 0;
-    const size_t sm = line_smem(L.nt, mode == 1 || (mode == 0 && exact_rings > 0), T);
+    const size_t sm = line_smem(L.nt, mode == 1 || (mode == 0 && exact_rings > 0), T, mode == 3);
     set_smem(k_circle<ON, K>, sm);
     launch_k(k_circle<ON, K>, dim3(lines, L.B), T, sm, st, L, u, f, cil, cm, corner, cz, of, parity,
              mode, exact_rings, active);
@@ -4377,7 +4397,7 @@ static void radial_k(const LevelView& L, double* u, const double* f, const doubl
                      const double* rm, int parity, bool serial, const int* active,
                      cudaStream_t st, int T, int lines) {
     const int mode = serial ? exact_mode(L.len) : 0;
-    const size_t sm = line_smem(L.len, mode == 1, T);
+    const size_t sm = line_smem(L.len, mode == 1, T, mode == 3);
     set_smem(k_radial<ON, K>, sm);
     launch_k(k_radial<ON, K>, dim3(lines, L.B), T, sm, st, L, u, f, ril, rm, parity, mode, active);
 }

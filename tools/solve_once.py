@@ -9,7 +9,9 @@ k = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 cyc = sys.argv[2] if len(sys.argv) > 2 else "V"
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 geom, prob, grid, st, meta = pmg.baseline_config(k, cycle=cyc)
-s = pmg.MultigridSolver(geom, prob, grid, st)
+B = meta["n_sections"]
+s = pmg.MultigridSolver(geom, prob, grid, st, n_sections=B,
+                        alpha_scales=pmg.section_scales(B) if B > 1 else None)
 s.seeded_rhs(20240611)
 for _ in range(n):
     r = s.solve()
