@@ -476,11 +476,39 @@ def run_gpu(args):
         "breakdown_one_solve": breakdown,
         "kernels_finest_level": kernels,
     }
+    if args.workload == "c3" and world == 1 and not args.no_extras:
+        # the single-grid config 2 (4097x4096, V and W cycles) beside the headline
+        solver.close()
+        line["extra"] = {w: single_grid_line(w, stream, local, torch, flush, not args.fast)
+                         for w in ("c2v", "c2w")}
     print(json.dumps(line))
     if dist:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def single_grid_line(workload, stream, local, torch, flush, reference_order, solves=2):
+    """Device-timed solves (1 warm-up + `solves`, L2 flushed between) of a
+    single-grid config: DOF*cycles/s, ms per solve, iterations."""
+    solver, _ = build_solver(workload, 0, 1, stream.cuda_stream, reference_order, device=local)
+    seeded(solver, workload, 0, None)
+    n = solver.n(0)
+    ms, its = [], 0
+    for i in range(1 + solves):
+        flush.add_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        rep = solver.solve()
+        b.record(stream)
+        torch.cuda.synchronize()
+        if i:
+            ms.append(a.elapsed_time(b))
+        its = rep.iterations
+    solver.close()
+    t = sum(ms) / len(ms)
+    return {"workload": WORKLOADS[workload][1], "value": n * its / (t * 1e-3), "unit": UNIT,
+            "ms_per_solve": round(t, 3), "iterations": its, "solves": solves}
 
 
 def ncu_traffic(workload, kind):
@@ -608,6 +636,8 @@ def main():
     ap.add_argument("--workload", default="c3", choices=list(WORKLOADS))
     ap.add_argument("--reps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the config-2 V/W lines added to the default c3 run")
     # default: line solves bitwise the reference's (the parity contract);
     # --fast: chunked parallel scans (roundoff-level drift from the reference)
     ap.add_argument("--fast", action="store_true")

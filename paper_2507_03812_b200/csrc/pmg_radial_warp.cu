@@ -2,6 +2,8 @@
 // the kernel, its launch shape and dispatch.  Separate translation unit (it
 // shares pmg_lines.cuh with the other line kernels) so that it rebuilds in
 // seconds.
+#include <cuda_pipeline.h>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -16,6 +18,14 @@ namespace pmg {
 namespace {
 
 constexpr int kRadUnroll = PMG_RAD_UNROLL;
+// rows of a rhs gather in flight per lane.  Radial: 2 (120 registers, 16 warps
+// per SM; measured 3 or 4 rows at 144-158 registers and 12 warps: 1.26-1.27 ms
+// vs 1.11 ms; 3-4 rows with the +-1 operands taken by shuffles, 11 loads per
+// row: 1.23-1.43 ms).  Circle: 4 (0.341 -> 0.305 ms).
+#ifndef PMG_CIRC_UNROLL
+#define PMG_CIRC_UNROLL 4
+#endif
+constexpr int kCircUnroll = PMG_CIRC_UNROLL;
 
 // ---------------------------------------------- warp-per-line radial sweep
 // Many radial lines of at most 32*KW nodes (config 3: 65536 spokes of 431
@@ -198,14 +208,27 @@ __global__ void __launch_bounds__(128) k_radial_warp(LevelView L, double* __rest
         R.rkp = L.rk[t];
     }
     const CoefAt<ONFLY> cf{&L, off, b};
-    // factors of the line and the identity padding
+    // factors of the line (asynchronous copies, in flight under the rhs
+    // gather) and the identity padding
 #pragma unroll 4
     for (int i = lane; i < stride; i += 32) {
-        Ld[i] = i < len ? ril[fo + i] : 1.0;
-        Mp[i + 1] = i < len - 1 ? rm[fo + i] : 0.0;
+        if (i < len)
+            __pipeline_memcpy_async(&Ld[i], &ril[fo + i], 8);
+        else
+            Ld[i] = 1.0;
+        if (i < len - 1)
+            __pipeline_memcpy_async(&Mp[i + 1], &rm[fo + i], 8);
+        else
+            Mp[i + 1] = 0.0;
         if (i >= len) Y[i] = 0.0;
     }
+    __pipeline_commit();
     if (lane == 0) Mp[0] = 0.0;
+#ifdef PMG_DIAG_NOGATHER
+    if (true) {
+        for (int i = lane; i < len; i += 32) Y[i] = F[base + i];
+    } else
+#endif
     if (!ONFLY && !L.rows && len >= 4) {
         // Take: rows 1 .. len-3 are lean and branch-free -- the operands of
         // kRadUnroll rows are in flight per lane before any arithmetic; the
@@ -229,12 +252,15 @@ __global__ void __launch_bounds__(128) k_radial_warp(LevelView L, double* __rest
         for (int i = lane; i < len; i += 32)
             Y[i] = radial_rhs<ONFLY>(L, cf, U, F, off, t, base, R, i);
     }
+    __pipeline_wait_prior(0);
     __syncwarp();
     const int j0 = lane * KE;
     double y[KE];
 #pragma unroll
     for (int q = 0; q < KE; ++q) y[q] = Y[j0 + q];
+#ifndef PMG_DIAG_NOSOLVE
     warp_tri<KE, EXACT>(y, Ld, Mp);
+#endif
     __syncwarp();
 #pragma unroll
     for (int q = 0; q < KE; ++q) Y[j0 + q] = y[q];
@@ -284,20 +310,27 @@ __global__ void __launch_bounds__(128) k_circle_warp(LevelView L, double* __rest
     double* Mp = Ld + stride;  // stride + 1 entries
 #pragma unroll 4
     for (int i = lane; i < stride; i += 32) {
-        Ld[i] = i < nt ? cil[fo + i] : 1.0;
-        Mp[i + 1] = i < nt - 1 ? cm[fo + i] : 0.0;
+        if (i < nt)
+            __pipeline_memcpy_async(&Ld[i], &cil[fo + i], 8);
+        else
+            Ld[i] = 1.0;
+        if (i < nt - 1)
+            __pipeline_memcpy_async(&Mp[i + 1], &cm[fo + i], 8);
+        else
+            Mp[i + 1] = 0.0;
         if (i >= nt) Y[i] = 0.0;
     }
+    __pipeline_commit();
     if (lane == 0) Mp[0] = 0.0;
     if (circle_lean_ring(L, s)) {
         const double hm = L.h[s - 1], rhm = L.rh[s - 1], hp = L.h[s], rhp = L.rh[s];
-        for (int t0 = lane; t0 < nt; t0 += 32 * kRadUnroll) {
-            CircOps o[kRadUnroll];
+        for (int t0 = lane; t0 < nt; t0 += 32 * kCircUnroll) {
+            CircOps o[kCircUnroll];
 #pragma unroll
-            for (int q = 0; q < kRadUnroll; ++q)
+            for (int q = 0; q < kCircUnroll; ++q)
                 if (t0 + 32 * q < nt) circ_load<false>(L, off, s, t0 + 32 * q, U, F, o[q]);
 #pragma unroll
-            for (int q = 0; q < kRadUnroll; ++q)
+            for (int q = 0; q < kCircUnroll; ++q)
                 if (t0 + 32 * q < nt) Y[t0 + 32 * q] = circ_eval(o[q], hm, rhm, hp, rhp);
         }
     } else {
@@ -320,6 +353,7 @@ __global__ void __launch_bounds__(128) k_circle_warp(LevelView L, double* __rest
             Y[t] = acc;
         }
     }
+    __pipeline_wait_prior(0);
     __syncwarp();
     const int j0 = lane * KE;
     double y[KE];
