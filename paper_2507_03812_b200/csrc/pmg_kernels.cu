@@ -1996,7 +1996,9 @@ __device__ __forceinline__ void circle_body(const LevelView& L, double* __restri
             for (int t = threadIdx.x; t < nt; t += T) RC[P(t)] = __drcp_rn(IL[P(t)]);
         __syncthreads();
         KT(3);
-        if (exact && par_ex)
+        if (exact && par_ex && nt <= 8 * T)
+            line_solve_ex<8, true>(Y, IL, RC, M, nt, corner[(long)b * L.split + s], cz + fo, scr);
+        else if (exact && par_ex)
             line_solve_ex<kExChunk, true>(Y, IL, RC, M, nt, corner[(long)b * L.split + s], cz + fo, scr);
         else if (serial == 3)
             line_solve_ex<kExChunk, true, true>(Y, IL, nullptr, M, nt, corner[(long)b * L.split + s],
@@ -2152,7 +2154,12 @@ __device__ __forceinline__ void radial_body(const LevelView& L, double* __restri
     __syncthreads();
     KT(3);
     if (serial == 1) {
-        line_solve_ex<kExChunk, false>(Y, IL, RC, M, len, 0.0, nullptr, scr);
+        // 8 rows per solving thread where the CTA covers the line that way
+        // (shorter dependent chains: c1 10.5 -> 9.5 ms), else 16
+        if (len <= 8 * T)
+            line_solve_ex<8, false>(Y, IL, RC, M, len, 0.0, nullptr, scr);
+        else
+            line_solve_ex<kExChunk, false>(Y, IL, RC, M, len, 0.0, nullptr, scr);
     } else if (serial == 3) {
         line_solve_ex<kExChunk, false, true>(Y, IL, nullptr, M, len, 0.0, nullptr, scr);
     } else if (serial) {
