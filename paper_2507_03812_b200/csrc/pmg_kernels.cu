@@ -4101,10 +4101,23 @@ inline size_t line_smem(int n, bool ex4 = false, int T = 512, bool ex3 = false) 
 // (line_solve_ex) when its four line arrays fit one CTA, else 2 = one thread
 // (line_solve_ex), 3 = the same with RN(1/l) evaluated on the fly (three line
 // arrays: 8192-node lines), 2 = one thread
-inline int exact_mode(int n) {
-    return line_smem(n, true) <= 227 * 1024                 ? 1
-           : line_smem(n, false, 512, true) <= 227 * 1024 ? 3
-                                                          : 2;
+// Radial lines (prefer3) also take mode 3 where it lets TWO lines be resident
+// per SM and mode 1 only one (2048..4096-node lines: one CTA's rhs gather then
+// overlaps the other's solve; c2-V radial 15.1 -> 12.5 ms).  Circle lines keep
+// mode 1: the across-origin ring's fast exact solve needs the fourth array
+// (measured 12.2 -> 19.7 ms in mode 3).  PMG_EXACT_MODE=1|3 forces a mode.
+inline int exact_mode(int n, bool prefer3 = false) {
+    static const int forced = [] {
+        const char* e = std::getenv("PMG_EXACT_MODE");
+        return e ? std::atoi(e) : 0;
+    }();
+    const int T = std::min(512, std::max(32, ((n + 15) / 16 + 31) / 32 * 32));  // 16 rows / thread
+    const size_t m1 = line_smem(n, true, T), m3 = line_smem(n, false, T, true);
+    const size_t cap = 227 * 1024, half = cap / 2 - 1024;
+    if (forced == 1 && m1 <= cap) return 1;
+    if (forced == 3 && m3 <= cap) return 3;
+    if (m1 <= cap && !(prefer3 && m1 > half && m3 <= half)) return 1;
+    return m3 <= cap ? 3 : 2;
 }
 
 }  // namespace
@@ -4403,7 +4416,7 @@ template <bool ON, int K>
 static void radial_k(const LevelView& L, double* u, const double* f, const double* ril,
                      const double* rm, int parity, bool serial, const int* active,
                      cudaStream_t st, int T, int lines) {
-    const int mode = serial ? exact_mode(L.len) : 0;
+    const int mode = serial ? exact_mode(L.len, true) : 0;
     const size_t sm = line_smem(L.len, mode == 1, T, mode == 3);
     set_smem(k_radial<ON, K>, sm);
     launch_k(k_radial<ON, K>, dim3(lines, L.B), T, sm, st, L, u, f, ril, rm, parity, mode, active);
