@@ -435,6 +435,12 @@ def run_gpu(args):
     kernels = {k: kernel_roofline(solver, k, peak, peak_kind, reps=20, workload=args.workload)
                for k in ("residual", "smooth", "circle", "radial")}
 
+    # which CUDA device each rank's solver ran on (LOCAL_RANK by construction)
+    devices = [local]
+    if dist:
+        got = [None] * world
+        dist.all_gather_object(got, local)
+        devices = got
     if rank != 0:
         if dist:
             dist.barrier()
@@ -463,7 +469,8 @@ def run_gpu(args):
         "dtype": "f64", "data": "synthetic (seeded U(-1,1) u*, f = A u*; random-free grid)",
         "config": config_dict(args.workload, world),
         "run_info": {"grid": f"{nr}x{nt}", "split": split, "levels": solver.num_levels(),
-                     "sections_per_rank": B, "iterations_first_sections": iters[:4] if iters else None,
+                     "sections_per_rank": B, "devices": devices,
+                     "iterations_first_sections": iters[:4] if iters else None,
                      "line_solves": "reference order (bitwise)" if not args.fast
                      else "chunked parallel scans"},
         "roofline": roof,
