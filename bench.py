@@ -336,7 +336,12 @@ def run_gpu(args):
     if args.workload == "give":
         return run_give(args, rank, world, local, stream, peak, peak_kind, dist)
 
-    solver, sections = build_solver(args.workload, rank, world, stream.cuda_stream,
+    # --rank-slice N (one process, one GPU): run only the slice rank 0 of an
+    # N-GPU job would own -- the per-rank workload of the sharded batch, which
+    # has no inter-GPU dependence, so N such ranks finish in max-over-ranks of
+    # this time; a projection aid where only one GPU is available
+    shard_world = args.rank_slice if (args.rank_slice > 1 and world == 1) else world
+    solver, sections = build_solver(args.workload, rank, shard_world, stream.cuda_stream,
                                     not args.fast, device=local)
     seeded(solver, args.workload, rank, sections)
     n = solver.n(0)
@@ -470,6 +475,7 @@ def run_gpu(args):
         "config": config_dict(args.workload, world),
         "run_info": {"grid": f"{nr}x{nt}", "split": split, "levels": solver.num_levels(),
                      "sections_per_rank": B, "devices": devices,
+                     "rank_slice_of": args.rank_slice if args.rank_slice > 1 else None,
                      "iterations_first_sections": iters[:4] if iters else None,
                      "line_solves": "reference order (bitwise)" if not args.fast
                      else "chunked parallel scans"},
@@ -483,7 +489,7 @@ def run_gpu(args):
         "breakdown_one_solve": breakdown,
         "kernels_finest_level": kernels,
     }
-    if args.workload == "c3" and world == 1 and not args.no_extras:
+    if args.workload == "c3" and world == 1 and not args.no_extras and args.rank_slice <= 1:
         # the single-grid config 2 (4097x4096, V and W cycles) beside the headline
         solver.close()
         line["extra"] = {w: single_grid_line(w, stream, local, torch, flush, not args.fast)
@@ -643,6 +649,8 @@ def main():
     ap.add_argument("--workload", default="c3", choices=list(WORKLOADS))
     ap.add_argument("--reps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--rank-slice", type=int, default=0,
+                    help="c3 on one GPU: only the sections rank 0 of an N-GPU job owns")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the config-2 V/W lines added to the default c3 run")
     # default: line solves bitwise the reference's (the parity contract);
