@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(128) k_circle_warp(LevelView L, double* __rest
 static int warp_kw(int n, long lines_total) {
     static const long min_lines = [] {
         const char* e = std::getenv("PMG_WARP_MIN_LINES");
-        return e ? std::atol(e) : 2048L;
+        return e ? std::atol(e) : 1024L;
     }();
     static const bool on = [] {
         const char* e = std::getenv("PMG_WARP_LINES");

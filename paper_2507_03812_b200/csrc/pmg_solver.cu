@@ -743,7 +743,16 @@ struct Solver {
             if (!fused_ok(V.v, serial, exact_rings)) continue;
             // large batches keep the per-colour launches (c3, 256 sections:
             // 14% slower fused -- ticket contention over 152K lines)
-            if ((long)B * (V.v.split + V.v.nt) > 16384) continue;
+            // batches whose lines run on the warp-per-line kernels keep the
+            // per-colour launches too: measured on the 32-section slice an
+            // 8-GPU rank owns, 20.7 -> 17.5 ms per solve (the fused step's
+            // CTA-per-line exact solves are slower than a warp per line)
+            if (B > 1 && !onfly && warp_batch_ok(V.v.len, (long)(V.v.nt / 2) * B)) continue;
+            static const long max_lines = [] {
+                const char* e = std::getenv("PMG_FUSED_MAX_LINES");
+                return e ? std::atol(e) : 16384L;
+            }();
+            if ((long)B * (V.v.split + V.v.nt) > max_lines) continue;
             if (!fuse_ctl) {
                 fuse_ctl = alloc<unsigned>(4);
                 const unsigned init[4] = {0u, 0u, 1u, 0u};
