@@ -3778,6 +3778,34 @@ __device__ __forceinline__ void exec_op(int op, const CoarseLevel& C, const Coar
                     if (j < n) a0 += A[(long)j * n + i] * C.f[off + j];
                     C.u[off + i] = a0 + a1;
                 }
+            } else if (env.n <= 32) {
+                // the reference's envelope substitutions (line_algebra.cpp:229-251)
+                // by one warp, lane i owning x_i: the forward sums run column by
+                // column (x_k final -> every row i > k with first_col <= k subtracts
+                // L(i,k) x_k), so each sum still receives its terms in increasing k,
+                // and the backward column updates are per element as written --
+                // the same operations on every x_i in the same order, bit for bit,
+                // in 2 n broadcast steps instead of ~2 nnz dependent ones
+                if (team.tid() < 32) {
+                    const int lane = team.tid(), n = env.n;
+                    const bool in = lane < n;
+                    const double* Lb = env.L + (long)bb * env.nnz;
+                    const int fi = in ? env.fc[lane] : 0;
+                    const double* ri = Lb + (in ? env.ro[lane] - fi : 0);
+                    double x = in ? C.f[off + lane] : 0.0;
+                    for (int k = 0; k < n; ++k) {
+                        const double xk = __shfl_sync(FULL, x, k);
+                        if (in && lane > k && fi <= k) x -= ri[k] * xk;
+                    }
+                    if (in) x /= env.D[(long)bb * n + lane];
+                    for (int i = n - 1; i >= 0; --i) {
+                        const double xi = __shfl_sync(FULL, x, i);
+                        const int fci = env.fc[i];
+                        const double* rr = Lb + env.ro[i] - fci;
+                        if (lane < i && lane >= fci) x -= rr[lane] * xi;
+                    }
+                    if (in) C.u[off + lane] = x;
+                }
             } else if (team.tid() == 0) {
                 double* x = C.u + off;
                 for (int k = 0; k < env.n; ++k) x[k] = C.f[off + k];
