@@ -3204,6 +3204,34 @@ __device__ __forceinline__ void warp_line_solve_ex(double (&y)[KW], const double
                                                    double corner, const double* __restrict__ z) {
     const int KE = (n + 31) >> 5;  // rows per lane (<= KW)
     const int lane = threadIdx.x & 31, j0 = lane * KE;
+    if (n <= 32) {
+        // one row per lane (the coarse tail's 4..32-node lines): the
+        // substitution itself, row by row, each result broadcast by a shuffle
+        // -- exact by construction, and for lines this short cheaper than the
+        // scan, the restart and up to n verification waves
+        const bool in = lane < n;
+        const double l = in ? Ld[lane] : 1.0, rc = __drcp_rn(l);
+        const double mp = (in && lane > 0) ? Mo[lane - 1] : 0.0;      // m_{j-1}
+        const double mn = (in && lane < n - 1) ? Mo[lane] : 0.0;      // m_j
+        double v = y[0];
+        if (lane == 0) v = xdiv(v, l, rc);
+        for (int k = 1; k < n; ++k) {
+            const double p = __shfl_sync(FULL, v, k - 1);
+            if (lane == k) v = xdiv(v - mp * p, l, rc);
+        }
+        if (lane == n - 1) v = xdiv(v, l, rc);
+        for (int k = n - 2; k >= 0; --k) {
+            const double p = __shfl_sync(FULL, v, k + 1);
+            if (lane == k) v = xdiv(v - mn * p, l, rc);
+        }
+        if (CYC) {
+            const double x0 = __shfl_sync(FULL, v, 0), xl = __shfl_sync(FULL, v, n - 1);
+            const double tau = corner * (x0 + xl) / (1.0 + corner * (z[0] + z[n - 1]));
+            if (in) v -= tau * z[lane];
+        }
+        y[0] = v;
+        return;
+    }
     const bool live = j0 < n;
     double b[KW];
 #pragma unroll
