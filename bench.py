@@ -457,7 +457,7 @@ def run_gpu(args):
             if args.workload == "c3":
                 thr = os.cpu_count() or 1
                 v, secs, cnt, sample, thr, _ = cpu_reference_solves(
-                    "c3", thr, sections=list(range(min(thr, 256))))
+                    "c3", thr, sections=list(range(min(8 * thr, 256))))  # ~10-20 s of CPU work
             else:
                 ns = 2 if args.workload in ("c1", "c0") else 1
                 v, secs, cnt, sample, thr, _ = cpu_reference_solves(args.workload, ns)
