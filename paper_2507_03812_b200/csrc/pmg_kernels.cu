@@ -1818,8 +1818,12 @@ __device__ __forceinline__ double tma_strip(const LevelView& L, const TmaGeom& G
     return v;
 }
 
-template <int MODE, bool NORM>
-__global__ void __launch_bounds__(288, PMG_TMA_MINB) k_apply_tma(LevelView L, TmaGeom G,
+// MINB: resident CTAs per SM the register allocation targets -- 2 (96
+// registers) for single large grids (tuned at 8193x8192), 3 (72 registers) for
+// batches of small sections, whose short strips leave more latency to cover
+// (256 x 513x512: 0.914 -> 0.874 ms)
+template <int MODE, bool NORM, int MINB = PMG_TMA_MINB>
+__global__ void __launch_bounds__(288, MINB) k_apply_tma(LevelView L, TmaGeom G,
                                                       const double* __restrict__ u,
                                                       const double* __restrict__ f,
                                                       double* __restrict__ out,
@@ -4221,9 +4225,15 @@ int launch_apply(const LevelView& L, bool onfly, int mode, const double* u, cons
         const TmaGeom S = tma_geom_auto(L);
 #define PMG_TMA(MO, NO)                                                                     \
     do {                                                                                    \
-        set_smem(k_apply_tma<MO, NO>, kTmaSmem);                                            \
-        launch_k(k_apply_tma<MO, NO>, dim3(S.cps * L.B), 288, kTmaSmem, st, L, S, u, f, out, \
-                 partials, norm_type, active);                                              \
+        if (L.B > 1) {                                                                      \
+            set_smem(k_apply_tma<MO, NO, 3>, kTmaSmem);                                     \
+            launch_k(k_apply_tma<MO, NO, 3>, dim3(S.cps * L.B), 288, kTmaSmem, st, L, S, u, \
+                     f, out, partials, norm_type, active);                                  \
+        } else {                                                                            \
+            set_smem(k_apply_tma<MO, NO>, kTmaSmem);                                        \
+            launch_k(k_apply_tma<MO, NO>, dim3(S.cps * L.B), 288, kTmaSmem, st, L, S, u, f, \
+                     out, partials, norm_type, active);                                     \
+        }                                                                                   \
     } while (0)
         if (mode == 0) {
             if (norm) PMG_TMA(0, true); else PMG_TMA(0, false);
